@@ -1,0 +1,125 @@
+"""CPU oracle — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2301_09310_b200``) never imports, links or executes it, and the two share no code.
+
+The arithmetic lives in ``oracle/oracle.c`` (plain full-matrix Gotoh, Eqs. 1-3,
+P:132-149; the seed-anchored EXTEND reading of SURVEY §8(c)); this module only marshals
+arguments through ctypes.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import time
+
+import numpy as np
+
+LOCAL, EXTEND = 0, 1
+OK, EINVALID_BASE, EEMPTY, ETOO_LARGE, EBAD_H0 = 0, -1, -2, -3, -4
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(path)
+        p, i, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int32, ctypes.c_int64
+        one = [p, i, p, i, i32, i32, i32, i32, i, i32, p]
+        lib.oracle_align_full.argtypes = one
+        lib.oracle_align_rows.argtypes = one
+        lib.oracle_tables.argtypes = [p, i, p, i, i32, i32, i32, i32, i, i32, p, p, p, p]
+        lib.oracle_align_batch.argtypes = [p, p, p, p, p, i64, i32, i32, i32, i32, i, p, p, p, p, i, i]
+        _LIB = lib
+    return _LIB
+
+
+def _b(s) -> bytes:
+    return s.encode() if isinstance(s, str) else bytes(s)
+
+
+def _buf(s: bytes):
+    return ctypes.c_char_p(s) if s else ctypes.c_char_p(b"\0")
+
+
+def align(q, t, match=1, mismatch=-4, alpha=7, beta=1, mode=LOCAL, h0=0, rows=False):
+    """(score, q_end, t_end) of one pair, or raises ValueError with the oracle status."""
+    q, t = _b(q), _b(t)
+    out = (ctypes.c_int32 * 3)()
+    fn = _lib().oracle_align_rows if rows else _lib().oracle_align_full
+    st = fn(_buf(q), len(q), _buf(t), len(t), match, mismatch, alpha, beta, mode, h0, out)
+    if st != OK:
+        raise ValueError(st)
+    return int(out[0]), int(out[1]), int(out[2])
+
+
+def tables(q, t, match=1, mismatch=-4, alpha=7, beta=1, mode=LOCAL, h0=0):
+    """Full H, E, F tables with the boundary: arrays of shape (m+1, n+1), index [i+1, j+1]."""
+    q, t = _b(q), _b(t)
+    n, m = len(q), len(t)
+    H = np.zeros((m + 1, n + 1), np.int32)
+    E = np.zeros_like(H)
+    F = np.zeros_like(H)
+    out = (ctypes.c_int32 * 3)()
+    st = _lib().oracle_tables(_buf(q), n, _buf(t), m, match, mismatch, alpha, beta, mode, h0,
+                              H.ctypes.data, E.ctypes.data, F.ctypes.data, out)
+    if st != OK:
+        raise ValueError(st)
+    return H, E, F, (int(out[0]), int(out[1]), int(out[2]))
+
+
+def align_batch(batch, match=1, mismatch=-4, alpha=7, beta=1, mode=LOCAL, threads=None, rows=False):
+    """Oracle over a synth.Batch-like object (q_ascii, q_off, t_ascii, t_off, h0).
+
+    Returns (score, q_end, t_end, status, threads_used) as numpy int32 arrays."""
+    n = len(batch.q_off) - 1
+    score = np.empty(n, np.int32)
+    qe = np.empty(n, np.int32)
+    te = np.empty(n, np.int32)
+    st = np.empty(n, np.int32)
+    threads = threads or os.cpu_count() or 1
+    qa = np.ascontiguousarray(batch.q_ascii)
+    ta = np.ascontiguousarray(batch.t_ascii)
+    qo = np.ascontiguousarray(batch.q_off, np.int64)
+    to = np.ascontiguousarray(batch.t_off, np.int64)
+    h0 = np.ascontiguousarray(batch.h0, np.int32)
+    used = _lib().oracle_align_batch(qa.ctypes.data, qo.ctypes.data, ta.ctypes.data, to.ctypes.data,
+                                     h0.ctypes.data, n, match, mismatch, alpha, beta, mode,
+                                     score.ctypes.data, qe.ctypes.data, te.ctypes.data, st.ctypes.data,
+                                     threads, int(rows))
+    return score, qe, te, st, used
+
+
+def timed_sample(batch, seconds=10.0, mode=LOCAL, threads=None, **sc):
+    """Time the oracle, as it stands, over a bounded prefix of `batch`, growing the prefix until
+    about `seconds` of wall time are spent.  Returns dict(gcups, cells, pairs, seconds, threads)."""
+    from synth import Batch  # shared input module only
+
+    threads = threads or os.cpu_count() or 1
+    n_total = len(batch.q_off) - 1
+    k = min(n_total, 64 * threads)
+    cells_tot, pairs_tot, t_tot = 0, 0, 0.0
+    start = 0
+    while t_tot < seconds and start < n_total:
+        end = min(n_total, start + k)
+        sub = Batch(batch.q_ascii, batch.q_off[start:end + 1], batch.t_ascii, batch.t_off[start:end + 1],
+                    batch.h0[start:end])
+        t0 = time.perf_counter()
+        _, _, _, _, used = align_batch(sub, mode=mode, threads=threads, **sc)
+        dt = time.perf_counter() - t0
+        ql = np.diff(sub.q_off).astype(np.int64)
+        tl = np.diff(sub.t_off).astype(np.int64)
+        cells_tot += int(np.dot(ql, tl))
+        pairs_tot += end - start
+        t_tot += dt
+        start = end
+        if dt < seconds / 8:
+            k *= 2
+    return dict(gcups=cells_tot / t_tot / 1e9 if t_tot > 0 else 0.0, cells=cells_tot, pairs=pairs_tot,
+                seconds=t_tot, threads=threads)

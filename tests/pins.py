@@ -1,0 +1,148 @@
+"""Independent formulations used to PIN the oracle (tests only; nothing here is imported by the
+oracle or by the product).  Each is a different mathematical route to the same quantity:
+
+* ``brute_local`` / ``brute_extend`` — enumerate every alignment path explicitly (exponential;
+  tiny inputs only).  Gap cost g(k) = alpha + (k-1) beta per maximal run of one gap type; an
+  insertion run followed by a deletion run is two gaps (SURVEY §8(c) "a gap may open after any
+  column").  LOCAL: paths start with a match/mismatch column anywhere, value = path score, cell
+  value = max(0, best path ending there) (Eq. 1 "0" term = empty alignment).  EXTEND:
+  paths start at the anchor (-1,-1) with total h0 and are killed the moment the running total
+  drops to <= 0 (SURVEY §8(c) brute-force definition).
+* ``wsb_local`` / ``wsb_extend`` — the cubic Waterman-Smith-Beyer recurrence with an explicit
+  general gap cost g(k) (no E/F auxiliary states at all).
+* ``kadane_gapfree`` — when alpha > match*min(m,n) no gap can ever help, and H on every
+  diagonal is Kadane's maximum-suffix recurrence H = max(0, H_prev + S).
+
+All return (score, q_end, t_end) with the tie rule of SPEC S:205/S:256 (max score, then smallest
+target index i, then smallest query index j) and the zero/anchor conventions of SURVEY §8(b).
+"""
+from __future__ import annotations
+
+import sys
+
+NEG = -(1 << 40)
+
+
+def subst(a: str, b: str, match: int, mismatch: int) -> int:
+    a, b = a.upper().replace("U", "T"), b.upper().replace("U", "T")
+    return match if (a == b and a != "N") else mismatch
+
+
+def _pick(cells: dict, floor: int, floor_pos: tuple[int, int]):
+    """cells: {(i, j): value}; returns (score, q_end, t_end) by the tie rule."""
+    best, bi, bj = floor, floor_pos[0], floor_pos[1]
+    for (i, j) in sorted(cells):
+        if cells[(i, j)] > best:
+            best, bi, bj = cells[(i, j)], i, j
+    return best, bj, bi
+
+
+def brute_local(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1):
+    n, m = len(q), len(t)
+    best: dict = {}
+    sys.setrecursionlimit(10000)
+
+    def rec(i, j, total, last):
+        key = (i, j)
+        if total > best.get(key, NEG):
+            best[key] = total
+        if i + 1 < m and j + 1 < n:
+            rec(i + 1, j + 1, total + subst(t[i + 1], q[j + 1], match, mismatch), "M")
+        if j + 1 < n:
+            rec(i, j + 1, total - (beta if last == "I" else alpha), "I")
+        if i + 1 < m:
+            rec(i + 1, j, total - (beta if last == "D" else alpha), "D")
+
+    for i in range(m):
+        for j in range(n):
+            rec(i, j, subst(t[i], q[j], match, mismatch), "M")
+    cells = {k: max(0, v) for k, v in best.items()}
+    for i in range(m):
+        for j in range(n):
+            cells.setdefault((i, j), 0)
+    return _pick(cells, 0, (0, 0))
+
+
+def brute_extend(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1, h0=10):
+    n, m = len(q), len(t)
+    best: dict = {}
+
+    def rec(i, j, total, last):
+        if i >= 0 and j >= 0 and total > best.get((i, j), NEG):
+            best[(i, j)] = total
+        if i + 1 < m and j + 1 < n:
+            nt = total + subst(t[i + 1], q[j + 1], match, mismatch)
+            if nt > 0:
+                rec(i + 1, j + 1, nt, "M")
+        if j + 1 < n:
+            nt = total - (beta if last == "I" else alpha)
+            if nt > 0:
+                rec(i, j + 1, nt, "I")
+        if i + 1 < m:
+            nt = total - (beta if last == "D" else alpha)
+            if nt > 0:
+                rec(i + 1, j, nt, "D")
+
+    rec(-1, -1, h0, None)
+    return _pick(best, h0, (-1, -1))
+
+
+def _g(k, alpha, beta):
+    return alpha + (k - 1) * beta
+
+
+def wsb_local(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1):
+    n, m = len(q), len(t)
+    H = [[0] * (n + 1) for _ in range(m + 1)]  # H[i+1][j+1]
+    for i in range(m):
+        for j in range(n):
+            v = max(0, H[i][j] + subst(t[i], q[j], match, mismatch))
+            for k in range(1, j + 2):
+                v = max(v, H[i + 1][j + 1 - k] - _g(k, alpha, beta))
+            for k in range(1, i + 2):
+                v = max(v, H[i + 1 - k][j + 1] - _g(k, alpha, beta))
+            H[i + 1][j + 1] = v
+    cells = {(i, j): H[i + 1][j + 1] for i in range(m) for j in range(n)}
+    return _pick(cells, 0, (0, 0))
+
+
+def wsb_extend(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1, h0=10):
+    n, m = len(q), len(t)
+    H = [[0] * (n + 1) for _ in range(m + 1)]
+    H[0][0] = h0
+    for j in range(n):
+        H[0][j + 1] = max(0, h0 - _g(j + 1, alpha, beta))
+    for i in range(m):
+        H[i + 1][0] = max(0, h0 - _g(i + 1, alpha, beta))
+    for i in range(m):
+        for j in range(n):
+            hd = H[i][j]
+            v = hd + subst(t[i], q[j], match, mismatch) if hd > 0 else 0
+            v = max(0, v)
+            for k in range(1, j + 2):
+                src = H[i + 1][j + 1 - k]
+                if src > 0:
+                    v = max(v, src - _g(k, alpha, beta))
+            for k in range(1, i + 2):
+                src = H[i + 1 - k][j + 1]
+                if src > 0:
+                    v = max(v, src - _g(k, alpha, beta))
+            H[i + 1][j + 1] = v
+    cells = {(i, j): H[i + 1][j + 1] for i in range(m) for j in range(n)}
+    return _pick(cells, h0, (-1, -1))
+
+
+def kadane_gapfree(q: str, t: str, match=1, mismatch=-4):
+    """LOCAL result when gaps can never help (alpha > match*min(m,n)): per diagonal Kadane."""
+    n, m = len(q), len(t)
+    cells = {}
+    for d in range(-(m - 1), n):  # d = j - i
+        run = 0
+        i0 = max(0, -d)
+        for i in range(i0, m):
+            j = i + d
+            if j >= n:
+                break
+            run = max(0, run + subst(t[i], q[j], match, mismatch))
+            cells[(i, j)] = run
+    return _pick(cells, 0, (0, 0))
