@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""bench.py — GCUPS of the batched affine-gap seed-extension hot path on 1..8 B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--mode local|extend]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
+    python bench.py --impl reference ...                      (the CPU oracle arm)
+
+One step = one pass of the whole hot path (pack A1 -> schedule A2 -> DP A3 ->
+write-back A4, + results gather to rank 0 when N > 1, A5) over one batch of synthetic input that
+is already resident in HBM.  Weak scaling: every rank owns a disjoint slice of a global batch of
+N x (config pairs) pairs (per-pair seeded generator, so slices are independent).  Inputs (ASCII,
+~400 MB for config 2) are larger than L2, so no flush is needed between steps.
+
+Prints ONE JSON line on rank 0 (see the keys below).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GCUPS (cell updates/s) at 1/2/4/8 B200; fraction of int-pipe peak"
+WORKLOADS = {
+    1: "config1: 1k pairs, 150 bp query vs 150-250 bp target, ~5% mutations",
+    2: "config2: 1M Illumina-like pairs, 150 bp reads vs 250 bp windows, 2% sub + small indels",
+    3: "config3: 500k pairs, query 100-1000 bp log-uniform (load-imbalance stress)",
+    4: "config4: 100k long-read pairs, 1-10 kbp, ~15% errors",
+    5: "config5: 10M length-skewed pairs (Fig. 3 histograms + long tails)",
+}
+# algorithmic int lane-ops per cell: 5 recurrence + 1 substitution + 1 running max
+OPS_PER_CELL = {"int32": 7.0, "int16x2": 3.5}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="saloba", choices=["saloba", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--pairs", type=int, default=None, help="pairs per GPU (default: the config's count)")
+    ap.add_argument("--mode", default="local", choices=["local", "extend"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--force-group", type=int, default=0)
+    ap.add_argument("--force-path", type=int, default=0)
+    ap.add_argument("--keep-order", type=int, default=0)
+    ap.add_argument("--grouped", action="store_true", help="config 5: components contiguous")
+    return ap.parse_args()
+
+
+# ---- clocks sampled during the timed region ----------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        if args.impl == "saloba":
+            torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if args.impl == "saloba" else "gloo")
+    elif args.impl == "saloba":
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def load_intpipe():
+    """Measured int-pipe lane-ops/clk/SM (tools/intpipe.cu, profiles/intpipe_b200.json)."""
+    path = os.path.join(ROOT, "profiles", "intpipe_b200.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["alu_lane_ops_per_clk_per_sm"]), "measured (profiles/intpipe_b200.json)"
+    except Exception:
+        return 64.0, "guide: alu pipe rt_SMSP=2 -> 16 lanes/clk/SMSP x 4 (B300_MICROARCH.md)"
+
+
+def cpu_baseline(batch, mode, seconds):
+    import oracle  # the oracle, as it stands (cpu_baseline leg)
+
+    r = oracle.timed_sample(batch, seconds=seconds, mode=mode)
+    return {"value": round(r["gcups"], 4), "unit": "GCUPS", "cores": r["threads"], "kind": "oracle",
+            "sample": f"first {r['pairs']} pairs of the same workload ({r['cells']:.3e} cells, "
+                      f"{r['seconds']:.1f} s, full-matrix C oracle, {r['threads']} threads)"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU oracle on the host cores, as it stands, on a bounded sample."""
+    import synth
+
+    if rank != 0:
+        return
+    mode = 0 if args.mode == "local" else 1
+    n_sample = 20_000 if args.config in (1, 2, 3, 5) else 200
+    b = synth.generate(args.config, min(n_sample, args.pairs or synth.CONFIG_PAIRS[args.config]), seed=args.config)
+    per_step = max(2.0, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
+    import oracle
+
+    for _ in range(args.warmup):
+        oracle.timed_sample(b, seconds=per_step / 4, mode=mode)
+    vals, cells, secs, thr, pairs = [], 0, 0.0, 0, 0
+    for _ in range(args.steps):
+        r = oracle.timed_sample(b, seconds=per_step, mode=mode)
+        vals.append(r["gcups"])
+        cells += r["cells"]
+        secs += r["seconds"]
+        thr = r["threads"]
+        pairs += r["pairs"]
+    value = cells / secs / 1e9
+    line = {"metric": METRIC, "impl": "reference", "value": round(value, 4), "unit": "GCUPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * secs / args.steps, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic", "config": {"workload": WORKLOADS[args.config], "mode": args.mode,
+                                            "sample": f"bounded prefix of the workload per step (~{per_step:.0f} s)"},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GCUPS", "cores": thr, "kind": "oracle",
+                             "sample": f"{pairs} pairs over {args.steps} steps"},
+            "e2e": {"value": round(value, 4), "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import build_native
+
+    if rank == 0 or world == 1:
+        build_native.build_all()
+    if world > 1:
+        dist.barrier()
+    import paper_2301_09310_b200 as sb
+    import synth
+
+    cfg = args.config
+    n = args.pairs or synth.CONFIG_PAIRS[cfg]
+    mode = sb.LOCAL if args.mode == "local" else sb.EXTEND
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    # this rank's slice of the global batch, generated straight into pinned host memory
+    pinned = {}
+
+    def alloc(name, nbytes):
+        t = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+        pinned[name] = t
+        return t.numpy()[:nbytes]
+
+    t0 = time.time()
+    batch = synth.generate(cfg, n, seed=cfg, first=rank * n, n_total=world * n, grouped=args.grouped, out=alloc)
+    gen_s = time.time() - t0
+    cells_rank = batch.cells()
+    max_q = int(batch.qlen.max())
+    qa = torch.from_numpy(batch.q_ascii).to(dev)
+    ta = torch.from_numpy(batch.t_ascii).to(dev)
+    qo = torch.from_numpy(batch.q_off).to(dev)
+    to = torch.from_numpy(batch.t_off).to(dev)
+    h0 = torch.from_numpy(batch.h0).to(dev)
+    opts = sb.Options(args.force_group, args.force_path, args.keep_order)
+    al = sb.Aligner(n, int(batch.q_off[-1]), int(batch.t_off[-1]), max_q, sb.BWA_MEM, mode, sb.PACK4, opts)
+    stream = torch.cuda.current_stream()
+    gather_buf = None
+    if world > 1:
+        gather_buf = [torch.empty((3, n), dtype=torch.int32, device=dev) for _ in range(world)] if rank == 0 else None
+
+    def step(dp_ev=None):
+        o = sb.Options(args.force_group, args.force_path, args.keep_order, dp_ev) if dp_ev else None
+        s, qe, te = al.run(qa, qo, ta, to, h0, options=o)
+        if world > 1:  # A5: results gathered to rank 0 (the only collective; none inside the DP)
+            dist.gather(al.out[:, :n], gather_buf if rank == 0 else None, dst=0)
+        return s
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st = al.status.cpu().tolist()
+    assert st[0] == -1 and st[1] == -1 and st[2] == -1, f"bad status {st}"
+
+    dp_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                 for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = sb.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for k in range(args.steps):
+        step(dp_events[k])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = sb.kernel_launches() - launches0
+    clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    dp_ms = [a.elapsed_time(b) for a, b in dp_events]
+    t = torch.tensor([ms, sum(dp_ms) / len(dp_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, dp_ms_avg = float(t[0]), float(t[1])
+    ms_per_step = ms_max / args.steps
+    total_cells = cells_rank * world
+    value = total_cells * args.steps / (ms_max * 1e-3) / 1e9
+
+    # ---- end-to-end through the host-buffer C-ABI entry point (H2D + pack + align + D2H) ----
+    e2e = None
+    if args.e2e_steps > 0:
+        hb = batch  # its ASCII buffers are views of pinned host memory
+        out = torch.empty((3, n), dtype=torch.int32, pin_memory=True).numpy()
+        sb.align_host(hb, sb.BWA_MEM, mode, opts, out=out)  # warm
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            _, _, _, hst = sb.align_host(hb, sb.BWA_MEM, mode, opts, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te2 = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te2, op=dist.ReduceOp.MAX)
+        e2e_val = total_cells * args.e2e_steps / (float(te2[0]) * 1e-3) / 1e9
+        h2d = int(len(batch.q_ascii) + len(batch.t_ascii) + 16 * (n + 1) + (4 * n if mode == sb.EXTEND else 0))
+        e2e = {"value": round(e2e_val, 2), "unit": "GCUPS", "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": 12 * n * world, "api": "saloba_align_host (pinned host ASCII in, host results out)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    csum = clocks.summary()
+    p_int, p_src = load_intpipe()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_mhz = csum["sm_mhz"] or 1965.0
+    path = "int32"  # round 1: every pair takes the int32 exact path
+    peak = sms * f_mhz * 1e6 * p_int / OPS_PER_CELL[path] / 1e9
+    achieved = cells_rank / (dp_ms_avg * 1e-3) / 1e9
+    roof = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GCUPS",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "dp_i32_kernel (all G bins of one call, CUDA events on the launching stream)",
+            "dp_share_of_step": round(dp_ms_avg / ms_per_step, 3),
+            "peak_derivation": f"{sms} SMs x {f_mhz:.0f} MHz (median under load) x {p_int:.0f} int lane-ops/clk/SM "
+                               f"[{p_src}] / {OPS_PER_CELL[path]} ops per cell ({path} path)"}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(batch, mode, args.cpu_seconds)
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": path, "data": "synthetic",
+        "config": {"workload": WORKLOADS[cfg], "mode": args.mode, "pairs_per_gpu": n,
+                   "cells_per_step": total_cells, "scoring": "match 1, mismatch -4, alpha 7, beta 1 (BWA-MEM-style)",
+                   "l2": "inputs larger than L2 (ASCII %.0f MB per GPU per step)" % ((len(batch.q_ascii) + len(batch.t_ascii)) / 1e6),
+                   "parallelism": f"pairs sharded over {world} GPU(s), results gathered to rank 0",
+                   "gen_seconds": round(gen_s, 1)},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": {"sm_mhz": csum["sm_mhz"], "sm_max_mhz": csum["sm_max_mhz"], "reasons": csum["reasons"]},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+/*
+ * saloba.h — C ABI of the B200-native batched affine-gap seed-extension library.
+ *
+ * The operation (§II-A, Eqs. 1-3):
+ * for every pair k, fill the DP table of query q (columns j = 0..n-1) against target t
+ * (rows i = 0..m-1, "reference at i and query at j") with
+ *
+ *     E(i,j) = max(H(i,j-1) - alpha, E(i,j-1) - beta)                     (Eq. 2)
+ *     F(i,j) = max(H(i-1,j) - alpha, F(i-1,j) - beta)                     (Eq. 3)
+ *     H(i,j) = max(0, E(i,j), F(i,j), H(i-1,j-1) + S(t_i, q_j))           (Eq. 1)
+ *
+ * with S = match if the bases are equal and not N, else mismatch (N never matches),
+ * and return the best score and its end coordinates: maximal score, then smallest target index
+ * i, then smallest query index j.
+ *
+ *   SALOBA_LOCAL  — Smith-Waterman local mode: boundary 0; score >= 0; ends (0,0) when score = 0
+ *                   (S:249).
+ *   SALOBA_EXTEND — seed-anchored extension ("extending to both directions from the
+ *                   found seeds"; exact reading in DESIGN.md §2 / SURVEY §8(c)): an anchor
+ *                   H(-1,-1) = h0 (the seed's score), leading-gap boundaries
+ *                   H(-1,j) = max(0, h0-alpha-beta*j), H(i,-1) = max(0, h0-alpha-beta*i), no fresh
+ *                   local starts (H(i-1,j-1) == 0 kills the diagonal), score = max(h0, max H),
+ *                   ends (-1,-1) when no cell exceeds h0.
+ *
+ * alpha ("gap_open") is the cost of a gap's FIRST base and beta ("gap_extend") of each further
+ * base, literal to Eqs. 2-3 (BWA-MEM o=6,e=1 is alpha=7, beta=1).
+ *
+ * Conventions for every entry point:
+ *   - Pointers marked [dev] are device pointers owned by the caller (e.g. torch tensors); the
+ *     library never frees them and allocates nothing on the hot path.  [host] are host pointers.
+ *   - `stream` is a cudaStream_t passed as void*; NULL means the legacy default stream.  Device
+ *     calls are asynchronous on `stream`; outputs are valid after the stream is synchronised.
+ *   - Host-checkable errors return a negative SALOBA_E* code synchronously and launch nothing.
+ *   - Data-dependent errors are reported through the [dev] int64 `status` word: the call sets
+ *     it to -1 (no error) or to the smallest offending index (atomicMin), readable after the
+ *     stream is synchronised.
+ *   - Thread-safe across host threads and streams; no global mutable state except a per-device
+ *     cache of occupancy numbers computed once.
+ */
+#ifndef SALOBA_H
+#define SALOBA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SALOBA_VERSION 1
+
+typedef struct {
+    int32_t match;      /* >= 1        */
+    int32_t mismatch;   /* <= -1        */
+    int32_t gap_open;   /* alpha: cost of a gap's first base; alpha >= beta   */
+    int32_t gap_extend; /* beta: cost of each further gap base; beta >= 1    */
+} saloba_scoring;
+
+typedef enum { SALOBA_LOCAL = 0, SALOBA_EXTEND = 1 } saloba_mode;
+
+/* Packed base formats:
+ *   SALOBA_PACK4: 8 bases per uint32, base p in nibble p%8 (least-significant nibble first),
+ *                 codes A=0 C=1 G=2 T/U=3 N=4, padding nibble 15.
+ *   SALOBA_PACK2: 16 bases per uint32, base p in bits 2(p%16)..+1, codes A=0 C=1 G=2 T/U=3;
+ *                 N is not representable (pack reports it as an invalid base); padding bits 0
+ *                 and never scored (lengths mask it). */
+typedef enum { SALOBA_PACK2 = 2, SALOBA_PACK4 = 4 } saloba_packing;
+
+enum {
+    SALOBA_OK = 0,
+    SALOBA_EINVAL = -1,       /* bad argument (null pointer, n < 0, bad scheme, bad enum)      */
+    SALOBA_ECUDA = -2,        /* a CUDA runtime call failed                                    */
+    SALOBA_EWORKSPACE = -3,   /* workspace too small for n_pairs                               */
+    SALOBA_EUNSUPPORTED = -4, /* no B200 (sm_100) device or a feature this build lacks         */
+};
+
+/* Per-call tuning / test / profiling knobs.  Pass NULL for the defaults (all zero). */
+typedef struct {
+    int32_t force_group;  /* 0: the scheduler picks the subwarp size G per pair; else G in {1,2,4,8,16,32}
+                             (pairs whose query exceeds that G's spill-row bound keep the scheduler's G) */
+    int32_t force_path;   /* 0: auto; 1: int32 exact path for every pair; 2: prefer the int16x2 path */
+    int32_t keep_order;   /* 1: do not sort pairs by length (A/B test of the scheduler)            */
+    int32_t reserved0;
+    void* ev_dp_begin;    /* optional cudaEvent_t recorded on `stream` right before the first DP
+                             kernel launch of the call (after packing/scheduling), for profiling */
+    void* ev_dp_end;      /* optional cudaEvent_t recorded on `stream` after the last DP kernel   */
+    int32_t reserved[4];
+} saloba_options;
+
+/* ---- A1: packing --------------------------------------------------------------------------- */
+
+/* Capacity (uint32 words) that saloba_pack needs for n_seqs sequences of total_bases bases.
+ * The packed layout is closed-form: sequence s starts at word byte_off[s]/B + s
+ * (B = 8 for PACK4, 16 for PACK2), so no scan is needed and every sequence is word-aligned. */
+int64_t saloba_packed_words(int64_t total_bases, int64_t n_seqs, saloba_packing fmt);
+
+/* ASCII {A,C,G,T,U,N; any case} -> packed words (SPEC S:44-52 pack_sequence).
+ *   ascii     [dev] uint8[byte_off[n_seqs]]      the concatenated sequences
+ *   byte_off  [dev] int64[n_seqs+1]              sequence s = ascii[byte_off[s] .. byte_off[s+1])
+ *   words     [dev] uint32[words_capacity]       output (see saloba_packed_words)
+ *   word_off  [dev] int64[n_seqs+1]              output: first word of each sequence (+ end)
+ *   lens      [dev] int32[n_seqs]                output: bases per sequence (may be NULL)
+ *   status    [dev] int64[1]                     -1, or the smallest byte index that is not a
+ *                                                valid base (InvalidBase; N under PACK2).
+ *                                                Empty sequences are legal here (0 words, lens 0);
+ *                                                saloba_align_batch reports them (EmptySequence).
+ * Returns SALOBA_OK or a negative code (nothing launched). */
+int saloba_pack(const uint8_t* ascii, const int64_t* byte_off, int64_t n_seqs, saloba_packing fmt,
+                uint32_t* words, int64_t words_capacity, int64_t* word_off, int32_t* lens, int64_t* status,
+                void* stream);
+
+/* ---- A2-A4: schedule, DP, write-back ------------------------------------------------------- */
+
+/* Device workspace (bytes) saloba_align_batch needs for n_pairs pairs whose query lengths are
+ * <= max_qlen (target lengths are unbounded up to 2^20; max_tlen is accepted for forward
+ * compatibility).  device = CUDA ordinal whose SM count sizes the persistent grids. */
+size_t saloba_workspace_bytes(int64_t n_pairs, int32_t max_qlen, int32_t max_tlen, int device);
+
+/* Align n_pairs packed pairs.
+ *   q_words, t_words        [dev] packed sequences (format fmt)
+ *   q_word_off, t_word_off  [dev] int64[n_pairs]  first word of pair k's query / target
+ *   q_len, t_len            [dev] int32[n_pairs]  lengths in bases (1 .. 2^20)
+ *   h0                      [dev] int32[n_pairs]  EXTEND: initial (seed) score, 1 .. 2^29;
+ *                                                  must be NULL-free in EXTEND, ignored in LOCAL
+ *   score, q_end, t_end     [dev] int32[n_pairs]  results, in INPUT order (SoA)
+ *   workspace               [dev] >= saloba_workspace_bytes(...) bytes, 256-byte aligned
+ *   status                  [dev] int64[1]        -1, or the smallest pair index with invalid
+ *                                                  data (length 0 or > 2^20, query longer than the
+ *                                                  workspace was sized for, h0 out of range);
+ *                                                  such pairs get score = -1, q_end = t_end = -2
+ *   opt                     [host] may be NULL
+ * Host-checked: pointers, n_pairs >= 0, scheme (match >= 1, mismatch <= -1, alpha >= beta >= 1,
+ * all |values| <= 2^10), mode/fmt enums, workspace size.
+ * Results are bit-identical regardless of G, precision path, batch order and sharding. */
+int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word_off, const int32_t* q_len,
+                       const uint32_t* t_words, const int64_t* t_word_off, const int32_t* t_len,
+                       const int32_t* h0, int64_t n_pairs, saloba_scoring sc, saloba_mode mode,
+                       saloba_packing fmt, int32_t* score, int32_t* q_end, int32_t* t_end, void* workspace,
+                       size_t workspace_bytes, int64_t* status, const saloba_options* opt, void* stream);
+
+/* ---- end-to-end from host buffers ----------------------------------------------------------- */
+
+/* Host-resident ASCII pairs in, host results out: uploads in pipelined slices (pinned host
+ * memory recommended), packs, aligns and downloads on `stream`, then synchronises it.
+ *   q_ascii, t_ascii  [host] uint8   concatenated sequences;  q_off, t_off [host] int64[n_pairs+1]
+ *   h0                [host] int32[n_pairs] or NULL in LOCAL
+ *   score, q_end, t_end [host] int32[n_pairs]
+ *   host_status       [host] int64: -1 or smallest bad pair index (invalid base / empty / length)
+ * Device memory is allocated and freed inside the call (this entry point is the convenience
+ * API; the device entry points above are the allocation-free hot path). */
+int saloba_align_host(const uint8_t* q_ascii, const int64_t* q_off, const uint8_t* t_ascii, const int64_t* t_off,
+                      const int32_t* h0, int64_t n_pairs, saloba_scoring sc, saloba_mode mode, int32_t* score,
+                      int32_t* q_end, int32_t* t_end, int64_t* host_status, const saloba_options* opt,
+                      void* stream);
+
+/* Static description of an error code. */
+const char* saloba_strerror(int code);
+
+/* SALOBA_VERSION of the built library. */
+int saloba_version(void);
+
+/* Diagnostics: number of this library's own kernels launched so far in this process (all devices;
+ * CUB radix-sort launches are not counted).  Process-wide atomic counter. */
+int64_t saloba_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SALOBA_H */

@@ -106,7 +106,9 @@ def timed_sample(batch, seconds=10.0, mode=LOCAL, threads=None, **sc):
     k = min(n_total, 64 * threads)
     cells_tot, pairs_tot, t_tot = 0, 0, 0.0
     start = 0
-    while t_tot < seconds and start < n_total:
+    while t_tot < seconds:
+        if start >= n_total:  # wrap around: the sample is re-used until the time budget is spent
+            start = 0
         end = min(n_total, start + k)
         sub = Batch(batch.q_ascii, batch.q_off[start:end + 1], batch.t_ascii, batch.t_off[start:end + 1],
                     batch.h0[start:end])

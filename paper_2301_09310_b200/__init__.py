@@ -1,0 +1,289 @@
+"""paper_2301_09310_b200 — B200-native batched affine-gap seed extension (SALoBa hot path).
+
+Thin Python binding over the C ABI in ``include/saloba.h`` (``libsaloba.so``, built in-tree for
+sm_100a).  Argument marshalling only: every step of the path (packing, scheduling, DP, write-back)
+runs in the library's CUDA kernels.  PyTorch supplies device memory and streams.  There is no CPU
+fallback: if the library is missing or no sm_100 device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+__all__ = [
+    "LOCAL", "EXTEND", "PACK4", "PACK2", "Scoring", "Options", "BWA_MEM", "SalobaError", "lib", "lib_path",
+    "packed_words", "pack", "workspace_bytes", "align_batch", "align", "align_host", "version", "EXPORTS",
+]
+
+LOCAL, EXTEND = 0, 1
+PACK2, PACK4 = 2, 4
+OK, EINVAL, ECUDA, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4
+
+#: every symbol include/saloba.h declares
+EXPORTS = ("saloba_packed_words", "saloba_pack", "saloba_workspace_bytes", "saloba_align_batch",
+           "saloba_align_host", "saloba_strerror", "saloba_version", "saloba_kernel_launches")
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libsaloba.so")
+_LIB = None
+
+
+class SalobaError(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        self.code = code
+        msg = lib().saloba_strerror(code).decode() if _LIB is not None else str(code)
+        super().__init__(f"{what}: {msg} ({code})" if what else f"{msg} ({code})")
+
+
+class _Scoring(ctypes.Structure):
+    _fields_ = [("match", ctypes.c_int32), ("mismatch", ctypes.c_int32), ("gap_open", ctypes.c_int32),
+                ("gap_extend", ctypes.c_int32)]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("force_group", ctypes.c_int32), ("force_path", ctypes.c_int32), ("keep_order", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32), ("ev_dp_begin", ctypes.c_void_p), ("ev_dp_end", ctypes.c_void_p),
+                ("reserved", ctypes.c_int32 * 4)]
+
+
+@dataclass(frozen=True)
+class Scoring:
+    """match >= 1, mismatch <= -1, gap_open = alpha (first gap base) >= gap_extend = beta >= 1."""
+
+    match: int = 1
+    mismatch: int = -4
+    gap_open: int = 7
+    gap_extend: int = 1
+
+    def _c(self) -> _Scoring:
+        return _Scoring(self.match, self.mismatch, self.gap_open, self.gap_extend)
+
+
+#: BWA-MEM-style scoring of the BASELINE configs: match 1, mismatch -4, o=6 e=1 -> alpha 7, beta 1
+BWA_MEM = Scoring(1, -4, 7, 1)
+
+
+@dataclass(frozen=True)
+class Options:
+    force_group: int = 0  # 0 = scheduler; else G in {1,2,4,8,16,32}
+    force_path: int = 0  # 0 auto, 1 int32 exact, 2 prefer int16x2
+    keep_order: int = 0  # 1 = no length sort
+    dp_events: tuple | None = None  # (torch.cuda.Event, torch.cuda.Event) bracketing the DP kernels
+
+    def _c(self) -> _Options:
+        o = _Options(self.force_group, self.force_path, self.keep_order, 0)
+        if self.dp_events is not None:
+            o.ev_dp_begin = ctypes.c_void_p(self.dp_events[0].cuda_event)
+            o.ev_dp_end = ctypes.c_void_p(self.dp_events[1].cuda_event)
+        return o
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded C-ABI library (raises if it was not built)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(lib_path):
+            raise ImportError(f"{lib_path} is missing; build it with `python build_native.py` "
+                              "(or __graft_entry__.build()). There is no CPU fallback.")
+        L = ctypes.CDLL(lib_path)
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        L.saloba_packed_words.argtypes = [i64, i64, ctypes.c_int]
+        L.saloba_packed_words.restype = i64
+        L.saloba_pack.argtypes = [vp, vp, i64, ctypes.c_int, vp, i64, vp, vp, vp, vp]
+        L.saloba_pack.restype = ctypes.c_int
+        L.saloba_workspace_bytes.argtypes = [i64, i32, i32, ctypes.c_int]
+        L.saloba_workspace_bytes.restype = ctypes.c_size_t
+        L.saloba_align_batch.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, _Scoring, ctypes.c_int, ctypes.c_int,
+                                         vp, vp, vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(_Options), vp]
+        L.saloba_align_batch.restype = ctypes.c_int
+        L.saloba_align_host.argtypes = [vp, vp, vp, vp, vp, i64, _Scoring, ctypes.c_int, vp, vp, vp, vp,
+                                        ctypes.POINTER(_Options), vp]
+        L.saloba_align_host.restype = ctypes.c_int
+        L.saloba_strerror.argtypes = [ctypes.c_int]
+        L.saloba_strerror.restype = ctypes.c_char_p
+        L.saloba_version.restype = ctypes.c_int
+        L.saloba_kernel_launches.restype = ctypes.c_int64
+        _LIB = L
+    return _LIB
+
+
+def version() -> int:
+    return lib().saloba_version()
+
+
+def kernel_launches() -> int:
+    """Process-wide count of this library's own kernel launches (diagnostics; bench gpu_launches)."""
+    return int(lib().saloba_kernel_launches())
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != OK:
+        raise SalobaError(rc, what)
+
+
+def _p(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev_tensor(t: torch.Tensor, dtype, name: str) -> torch.Tensor:
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    return t.contiguous()
+
+
+def packed_words(total_bases: int, n_seqs: int, fmt: int = PACK4) -> int:
+    return int(lib().saloba_packed_words(total_bases, n_seqs, fmt))
+
+
+def pack(ascii: torch.Tensor, byte_off: torch.Tensor, fmt: int = PACK4, total_bases: int | None = None,
+         stream=None):
+    """ASCII (uint8, cuda) + byte offsets (int64[n+1], cuda) -> (words, word_off, lens, status).
+
+    ``status`` is a 1-element int64 cuda tensor: -1 or the first invalid byte index."""
+    ascii = _dev_tensor(ascii, torch.uint8, "ascii")
+    byte_off = _dev_tensor(byte_off, torch.int64, "byte_off")
+    n = byte_off.numel() - 1
+    total = ascii.numel() if total_bases is None else total_bases
+    cap = packed_words(total, n, fmt)
+    dev = ascii.device
+    words = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    word_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    lens = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    status = torch.empty(1, dtype=torch.int64, device=dev)
+    _check(lib().saloba_pack(_p(ascii), _p(byte_off), n, fmt, _p(words), cap, _p(word_off), _p(lens), _p(status),
+                             _stream(stream)), "saloba_pack")
+    return words, word_off, lens[:n], status
+
+
+def workspace_bytes(n_pairs: int, max_qlen: int, max_tlen: int = 0, device: int | None = None) -> int:
+    dev = torch.cuda.current_device() if device is None else device
+    b = int(lib().saloba_workspace_bytes(n_pairs, max_qlen, max_tlen, dev))
+    if b == 0:
+        raise SalobaError(ECUDA, "saloba_workspace_bytes")
+    return b
+
+
+def align_batch(q_words, q_word_off, q_len, t_words, t_word_off, t_len, h0=None, scoring: Scoring = BWA_MEM,
+                mode: int = LOCAL, fmt: int = PACK4, out=None, workspace: torch.Tensor | None = None,
+                options: Options | None = None, max_qlen: int | None = None, stream=None):
+    """Align packed pairs on the GPU. Returns (score, q_end, t_end, status) cuda int32/int64 tensors.
+
+    `workspace` (uint8 cuda tensor) is allocated when omitted (sized from max_qlen, or from
+    q_len.max() with a device sync)."""
+    n = q_len.numel()
+    dev = q_len.device
+    if out is None:
+        out = torch.empty((3, max(n, 1)), dtype=torch.int32, device=dev)
+    score, q_end, t_end = out[0], out[1], out[2]
+    if workspace is None:
+        mq = int(q_len.max().item()) if (max_qlen is None and n > 0) else (max_qlen or 1)
+        workspace = torch.empty(workspace_bytes(n, mq, 0, dev.index), dtype=torch.uint8, device=dev)
+    status = torch.empty(1, dtype=torch.int64, device=dev)
+    opt = ctypes.byref(options._c()) if options is not None else None
+    if mode == EXTEND and h0 is None:
+        raise ValueError("EXTEND mode needs h0")
+    args = [q_words, q_word_off, q_len, t_words, t_word_off, t_len]
+    names = ["q_words", "q_word_off", "q_len", "t_words", "t_word_off", "t_len"]
+    dts = [torch.int32, torch.int64, torch.int32, torch.int32, torch.int64, torch.int32]
+    args = [_dev_tensor(a, d, nm) for a, d, nm in zip(args, dts, names)]
+    if h0 is not None:
+        h0 = _dev_tensor(h0, torch.int32, "h0")
+    rc = lib().saloba_align_batch(*[_p(a) for a in args], _p(h0), n, scoring._c(), mode, fmt, _p(score),
+                                  _p(q_end), _p(t_end), _p(workspace), workspace.numel(), _p(status), opt,
+                                  _stream(stream))
+    _check(rc, "saloba_align_batch")
+    return score[:n], q_end[:n], t_end[:n], status
+
+
+def align(q_ascii, q_off, t_ascii, t_off, h0=None, scoring: Scoring = BWA_MEM, mode: int = LOCAL,
+          fmt: int = PACK4, options: Options | None = None, max_qlen: int | None = None, workspace=None,
+          stream=None):
+    """Device-resident ASCII pairs -> (score, q_end, t_end, status): pack (A1) then align (A2-A4).
+    status: -1, or the first bad pair index from alignment; pack errors raise after a sync."""
+    qw, qwo, ql, qst = pack(q_ascii, q_off, fmt, stream=stream)
+    tw, two, tl, tst = pack(t_ascii, t_off, fmt, stream=stream)
+    res = align_batch(qw, qwo[:-1], ql, tw, two[:-1], tl, h0, scoring, mode, fmt, workspace=workspace,
+                      options=options, max_qlen=max_qlen, stream=stream)
+    return (*res[:3], res[3], qst, tst)
+
+
+def align_host(batch, scoring: Scoring = BWA_MEM, mode: int = LOCAL, options: Options | None = None,
+               out=None, stream=None):
+    """End-to-end from host buffers (numpy / pinned CPU tensors): returns numpy-like int32 arrays
+    (score, q_end, t_end) and the host status (-1 or first bad pair)."""
+    import numpy as np
+
+    def host_ptr(a):
+        if isinstance(a, torch.Tensor):
+            assert not a.is_cuda
+            return ctypes.c_void_p(a.data_ptr())
+        return ctypes.c_void_p(a.ctypes.data)
+
+    n = len(batch.q_off) - 1
+    if out is None:
+        out = np.empty((3, max(n, 1)), np.int32)
+    st = ctypes.c_int64(0)
+    opt = ctypes.byref(options._c()) if options is not None else None
+    qo = np.ascontiguousarray(batch.q_off, np.int64)
+    to = np.ascontiguousarray(batch.t_off, np.int64)
+    h0 = np.ascontiguousarray(batch.h0, np.int32) if mode == EXTEND else None
+    o = out if isinstance(out, np.ndarray) else out.numpy()
+    rc = lib().saloba_align_host(host_ptr(batch.q_ascii), host_ptr(qo), host_ptr(batch.t_ascii), host_ptr(to),
+                                 host_ptr(h0) if h0 is not None else None, n, scoring._c(), mode,
+                                 ctypes.c_void_p(o[0].ctypes.data), ctypes.c_void_p(o[1].ctypes.data),
+                                 ctypes.c_void_p(o[2].ctypes.data), ctypes.byref(st), opt, _stream(stream))
+    _check(rc, "saloba_align_host")
+    return o[0, :n], o[1, :n], o[2, :n], int(st.value)
+
+
+class Aligner:
+    """Preallocated device pipeline for repeated batches of the same capacity (the hot path the
+    bench times): pack (A1) -> schedule + DP + write-back (A2-A4), all on one stream, no host sync.
+
+    Capacity: n_pairs pairs, total_q / total_t ASCII bytes, queries up to max_qlen bases."""
+
+    def __init__(self, n_pairs: int, total_q: int, total_t: int, max_qlen: int, scoring: Scoring = BWA_MEM,
+                 mode: int = LOCAL, fmt: int = PACK4, options: Options | None = None, device=None):
+        self.dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.n, self.scoring, self.mode, self.fmt = n_pairs, scoring, mode, fmt
+        self.options = options
+        d = self.dev
+        qcap, tcap = packed_words(total_q, n_pairs, fmt), packed_words(total_t, n_pairs, fmt)
+        self.qcap, self.tcap = qcap, tcap
+        self.q_words = torch.empty(max(qcap, 1), dtype=torch.int32, device=d)
+        self.t_words = torch.empty(max(tcap, 1), dtype=torch.int32, device=d)
+        self.q_word_off = torch.empty(n_pairs + 1, dtype=torch.int64, device=d)
+        self.t_word_off = torch.empty(n_pairs + 1, dtype=torch.int64, device=d)
+        self.q_len = torch.empty(max(n_pairs, 1), dtype=torch.int32, device=d)
+        self.t_len = torch.empty(max(n_pairs, 1), dtype=torch.int32, device=d)
+        self.out = torch.empty((3, max(n_pairs, 1)), dtype=torch.int32, device=d)
+        self.status = torch.empty(4, dtype=torch.int64, device=d)  # [pack q, pack t, align, -]
+        self.ws = torch.empty(workspace_bytes(n_pairs, max_qlen, 0, d.index), dtype=torch.uint8, device=d)
+
+    def run(self, q_ascii, q_off, t_ascii, t_off, h0=None, options: Options | None = None, stream=None):
+        """Returns views (score, q_end, t_end) of the preallocated output (valid after sync)."""
+        L, st = lib(), _stream(stream)
+        n = self.n
+        _check(L.saloba_pack(_p(q_ascii), _p(q_off), n, self.fmt, _p(self.q_words), self.qcap, _p(self.q_word_off),
+                             _p(self.q_len), ctypes.c_void_p(self.status.data_ptr()), st), "saloba_pack")
+        _check(L.saloba_pack(_p(t_ascii), _p(t_off), n, self.fmt, _p(self.t_words), self.tcap, _p(self.t_word_off),
+                             _p(self.t_len), ctypes.c_void_p(self.status.data_ptr() + 8), st), "saloba_pack")
+        o = options if options is not None else self.options
+        opt = ctypes.byref(o._c()) if o is not None else None
+        rc = L.saloba_align_batch(_p(self.q_words), _p(self.q_word_off), _p(self.q_len), _p(self.t_words),
+                                  _p(self.t_word_off), _p(self.t_len), _p(h0) if self.mode == EXTEND else None, n,
+                                  self.scoring._c(), self.mode, self.fmt, _p(self.out[0]), _p(self.out[1]),
+                                  _p(self.out[2]), _p(self.ws), self.ws.numel(),
+                                  ctypes.c_void_p(self.status.data_ptr() + 16), opt, st)
+        _check(rc, "saloba_align_batch")
+        return self.out[0, :n], self.out[1, :n], self.out[2, :n]

@@ -1,0 +1,96 @@
+// common.cuh — shared device-side definitions of the saloba library (product path only).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "saloba.h"
+
+#define SALOBA_API extern "C" __attribute__((visibility("default")))
+
+namespace saloba {
+
+// process-wide count of this library's own kernel launches (saloba_kernel_launches)
+void count_launches(int n);
+
+// ---- bins ------------------------------------------------------------------------------------
+// bin = path * 8 + gidx; gidx = log2(G) (G in {1,2,4,8,16,32}); path 0 = int32 exact kernel,
+// path 1 = int16x2 pair-SIMD two-pass kernel.  Bin 15 collects invalid pairs (never launched).
+constexpr int NBINS = 16;
+constexpr int BIN_SKIP = 15;
+constexpr int PATH_I32 = 0, PATH_I16 = 1;
+constexpr int NGROUPS = 6;
+// Largest query block count Q = ceil(qlen/8) a bin of group size G accepts: bounds the spill pool
+// (one chunk-boundary row per subwarp slot).  G = 32 takes everything up to the batch maximum.
+__host__ __device__ constexpr int qmax_for_gidx(int gidx) {
+    return gidx == 0 ? 40 : gidx == 1 ? 80 : gidx == 2 ? 160 : gidx == 3 ? 320 : gidx == 4 ? 1280 : (1 << 17);
+}
+constexpr int MAX_LEN = 1 << 20;   // S:151 overflow envelope for int32 cells
+constexpr int MAX_H0 = 1 << 29;
+constexpr int BLOCK_THREADS = 256;
+
+struct SortKV {
+    uint64_t* keys_in;
+    uint64_t* keys_out;
+    uint32_t* vals_in;
+    uint32_t* vals_out;
+    void* cub_temp;
+    size_t cub_temp_bytes;
+};
+
+struct ClassifyArgs {
+    const int32_t* q_len;
+    const int32_t* t_len;
+    const int32_t* h0;
+    int64_t n;
+    int mode;
+    int force_gidx;   // -1 = auto
+    int force_path;   // 0 auto, 1 int32, 2 int16x2 preferred
+    int keep_order;
+    int64_t max_q_supported;  // query length the spill pool was sized for
+    int32_t* score;
+    int32_t* q_end;
+    int32_t* t_end;
+    uint64_t* keys;
+    uint32_t* vals;
+    int32_t* bin_count;  // [NBINS]
+    unsigned long long* status;
+};
+
+// Everything a DP kernel needs; passed by value.
+struct AlignArgs {
+    const uint32_t* q_words;
+    const int64_t* q_word_off;
+    const int32_t* q_len;
+    const uint32_t* t_words;
+    const int64_t* t_word_off;
+    const int32_t* t_len;
+    const int32_t* h0;
+    int64_t n_pairs;
+    int32_t match, mismatch, alpha, beta;
+    int32_t fmt;  // 4 or 2
+    int32_t* score;
+    int32_t* q_end;
+    int32_t* t_end;
+    const uint32_t* perm;     // sorted position -> input index
+    const int32_t* bin_start; // [NBINS + 1]
+    int32_t* bin_counter;     // [NBINS] dynamic work queues
+    int32_t* spill;           // pool (int32 view)
+    int64_t spill_stride;     // elements per (slot, buffer, H|F) row
+};
+
+// 8 consecutive bases [8w, 8w+8) of a packed sequence as 8 nibbles (base c in nibble c).
+// PACK4: one word.  PACK2: half of a word expanded to nibbles (no N, no padding code: the caller
+// masks by length).
+__device__ __forceinline__ uint32_t load_block8(const uint32_t* __restrict__ words, int w, int fmt) {
+    if (fmt == SALOBA_PACK4) return __ldg(words + w);
+    uint32_t x = __ldg(words + (w >> 1)) >> ((w & 1) * 16);  // 8 x 2-bit codes in the low 16 bits
+    // spread 2-bit fields into 4-bit nibbles
+    uint32_t r = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) r |= ((x >> (2 * c)) & 3u) << (4 * c);
+    return r;
+}
+
+__device__ __forceinline__ int nib(uint32_t w, int c) { return (w >> (4 * c)) & 15; }
+
+}  // namespace saloba

@@ -1,0 +1,216 @@
+// dp_i32.cu — A3 (int32 exact path): anti-diagonal wavefront DP over a subwarp of G lanes per pair.
+//
+// Decomposition (§IV-A): the DP table is cut into 8x8-cell
+// blocks (one packed word of each sequence).  A strip is a row of blocks (8 target
+// rows); a chunk is G strips, one per lane.  At step s lane k computes block (strip k, column
+// w = s - k), so a chunk takes Q + G - 1 steps ("Q + 31" for G = 32).
+// Dependencies (Fig. 4(c)): the left column (H, E of 8 rows) and the top-left
+// corner stay in registers; the top row (H, F of 8 columns) comes from lane k-1's previous step
+// through __shfl_up_sync (the paper used shared memory; §VII-A found them equivalent).
+// Only chunk-bottom rows leave the SM: lane G-1 writes them to a per-subwarp spill row
+// that lane 0 of the next chunk reads (double-buffered by chunk parity).
+//
+// Best-cell tracking is exact and in-pass: per row, a strict '>' keeps the first column reaching
+// the row maximum; chunk end reduces rows -> lanes (lexicographic value desc, i asc, j asc) and a
+// strict '>' across chunks keeps the earliest rows.
+// This path handles everything (N anywhere, both modes, the full int32 envelope of S:151) and is
+// the route for pairs the int16x2 path cannot take.
+#include <climits>
+
+#include "common.cuh"
+
+namespace saloba {
+
+template <int G, int MODE>
+__global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int bin) {
+    const int lane = threadIdx.x & 31;
+    const int k = lane & (G - 1);
+    const int sub_base = lane & ~(G - 1);
+    const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << sub_base);
+    const int64_t slot = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+    int32_t* const spill = a.spill + slot * 4 * a.spill_stride;
+
+    const int start = a.bin_start[bin];
+    const int cnt = a.bin_start[bin + 1] - start;
+    const int al = a.alpha, be = a.beta, ma = a.match, mm = a.mismatch;
+
+    for (;;) {
+        int item = 0;
+        if (k == 0) item = atomicAdd(a.bin_counter + bin, 1);
+        item = __shfl_sync(mask, item, 0, G);
+        if (item >= cnt) break;
+        const int p = int(a.perm[start + item]);
+        const int n = a.q_len[p], m = a.t_len[p];
+        const int h0 = MODE ? a.h0[p] : 0;
+        const uint32_t* __restrict__ qw = a.q_words + a.q_word_off[p];
+        const uint32_t* __restrict__ tw = a.t_words + a.t_word_off[p];
+        const int Q = (n + 7) >> 3, strips = (m + 7) >> 3, chunks = (strips + G - 1) / G;
+
+        int bestv = MODE ? h0 : 0, besti = MODE ? -1 : 0, bestj = MODE ? -1 : 0;
+
+        for (int c = 0; c < chunks; ++c) {
+            const int strip = c * G + k, r0 = strip * 8;
+            const int32_t* rdH = spill + ((c & 1) ^ 1) * 2 * a.spill_stride;
+            const int32_t* rdF = rdH + a.spill_stride;
+            int32_t* wrH = spill + (c & 1) * 2 * a.spill_stride;
+            int32_t* wrF = wrH + a.spill_stride;
+
+            // target codes of my 8 rows; rows past m and N never match (0xFF)
+            const uint32_t tword = (strip < strips) ? load_block8(tw, strip, a.fmt) : 0u;
+            int tc[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int code = nib(tword, r);
+                tc[r] = (r0 + r < m && code < 4) ? code : 0xFF;
+            }
+            int Hl[8], El[8], bv[8], bc[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                Hl[r] = MODE ? max(0, h0 - al - be * (r0 + r)) : 0;  // H(i,-1)
+                El[r] = 0;                                            // E(i,-1)
+                bv[r] = MODE ? h0 : 0;                                // only cells beating this count
+                bc[r] = -1;
+            }
+            int corner = MODE ? (r0 == 0 ? h0 : max(0, h0 - al - be * (r0 - 1))) : 0;  // H(r0-1, -1)
+            int botH[8], botF[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) botH[x] = botF[x] = 0;
+
+            const int steps = Q + G - 1;
+            for (int s = 0; s < steps; ++s) {
+                const int w = s - k;
+                int topH[8], topF[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    topH[x] = __shfl_up_sync(mask, botH[x], 1, G);
+                    topF[x] = __shfl_up_sync(mask, botF[x], 1, G);
+                }
+                if (k == 0 && w < Q) {
+                    if (c == 0) {
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) {
+                            topH[x] = MODE ? max(0, h0 - al - be * (8 * w + x)) : 0;  // H(-1, j)
+                            topF[x] = 0;
+                        }
+                    } else {
+                        const int4* ph = reinterpret_cast<const int4*>(rdH + 8 * w);
+                        const int4* pf = reinterpret_cast<const int4*>(rdF + 8 * w);
+                        int4 h0v = ph[0], h1v = ph[1], f0v = pf[0], f1v = pf[1];
+                        topH[0] = h0v.x; topH[1] = h0v.y; topH[2] = h0v.z; topH[3] = h0v.w;
+                        topH[4] = h1v.x; topH[5] = h1v.y; topH[6] = h1v.z; topH[7] = h1v.w;
+                        topF[0] = f0v.x; topF[1] = f0v.y; topF[2] = f0v.z; topF[3] = f0v.w;
+                        topF[4] = f1v.x; topF[5] = f1v.y; topF[6] = f1v.z; topF[7] = f1v.w;
+                    }
+                }
+                if (w >= 0 && w < Q && r0 < m) {
+                    const uint32_t qword = load_block8(qw, w, a.fmt);
+                    int qc[8];
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) qc[x] = (8 * w + x < n) ? nib(qword, x) : 15;
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        int hup = topH[x], fup = topF[x];
+                        int hdiag = (x == 0) ? corner : topH[x - 1];
+                        const int col = 8 * w + x;
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            const int e = max(Hl[r] - al, El[r] - be);
+                            const int f = max(hup - al, fup - be);
+                            int d = hdiag + ((tc[r] == qc[x]) ? ma : mm);
+                            if (MODE) d = (hdiag > 0) ? d : 0;
+                            const int h = max(max(0, e), max(f, d));
+                            if (h > bv[r]) {
+                                bv[r] = h;
+                                bc[r] = col;
+                            }
+                            hdiag = Hl[r];
+                            Hl[r] = h;
+                            El[r] = e;
+                            hup = h;
+                            fup = f;
+                        }
+                        botH[x] = hup;
+                        botF[x] = fup;
+                    }
+                    corner = topH[7];
+                    if (k == G - 1 && c + 1 < chunks) {
+                        int4* ph = reinterpret_cast<int4*>(wrH + 8 * w);
+                        int4* pf = reinterpret_cast<int4*>(wrF + 8 * w);
+                        ph[0] = make_int4(botH[0], botH[1], botH[2], botH[3]);
+                        ph[1] = make_int4(botH[4], botH[5], botH[6], botH[7]);
+                        pf[0] = make_int4(botF[0], botF[1], botF[2], botF[3]);
+                        pf[1] = make_int4(botF[4], botF[5], botF[6], botF[7]);
+                    }
+                }
+            }
+            // lane best: max value, then smallest row (rows ascend), column already first-max
+            int lv = MODE ? h0 : 0, li = INT_MAX, lj = INT_MAX;
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                if (bc[r] >= 0 && bv[r] > lv) {
+                    lv = bv[r];
+                    li = r0 + r;
+                    lj = bc[r];
+                }
+            // subwarp reduction: (value desc, i asc, j asc)
+#pragma unroll
+            for (int off = 1; off < G; off <<= 1) {
+                const int ov = __shfl_xor_sync(mask, lv, off, G);
+                const int oi = __shfl_xor_sync(mask, li, off, G);
+                const int oj = __shfl_xor_sync(mask, lj, off, G);
+                const bool take = (ov > lv) || (ov == lv && (oi < li || (oi == li && oj < lj)));
+                if (take) {
+                    lv = ov;
+                    li = oi;
+                    lj = oj;
+                }
+            }
+            if (li != INT_MAX && lv > bestv) {
+                bestv = lv;
+                besti = li;
+                bestj = lj;
+            }
+            __syncwarp(mask);  // spill row written by lane G-1 is read by lane 0 next chunk
+        }
+        if (k == 0) {
+            a.score[p] = bestv;
+            a.q_end[p] = bestj;
+            a.t_end[p] = besti;
+        }
+    }
+}
+
+template <int MODE>
+static void launch_i32_mode(int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s) {
+    switch (gidx) {
+    case 0: dp_i32_kernel<1, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
+    case 1: dp_i32_kernel<2, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
+    case 2: dp_i32_kernel<4, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
+    case 3: dp_i32_kernel<8, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
+    case 4: dp_i32_kernel<16, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
+    default: dp_i32_kernel<32, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
+    }
+}
+
+void launch_dp_i32(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s) {
+    if (mode == SALOBA_EXTEND) launch_i32_mode<1>(gidx, grid, a, bin, s);
+    else launch_i32_mode<0>(gidx, grid, a, bin, s);
+    count_launches(1);
+}
+
+template <int MODE>
+static const void* kptr_mode(int gidx) {
+    switch (gidx) {
+    case 0: return (const void*)dp_i32_kernel<1, MODE>;
+    case 1: return (const void*)dp_i32_kernel<2, MODE>;
+    case 2: return (const void*)dp_i32_kernel<4, MODE>;
+    case 3: return (const void*)dp_i32_kernel<8, MODE>;
+    case 4: return (const void*)dp_i32_kernel<16, MODE>;
+    default: return (const void*)dp_i32_kernel<32, MODE>;
+    }
+}
+const void* dp_i32_kernel_ptr(int mode, int gidx) {
+    return mode == SALOBA_EXTEND ? kptr_mode<1>(gidx) : kptr_mode<0>(gidx);
+}
+
+}  // namespace saloba

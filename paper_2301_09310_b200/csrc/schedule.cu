@@ -1,0 +1,115 @@
+// schedule.cu — A2: length-aware scheduler (§III-A P:517-529 load imbalance; §IV-C
+// P:688-702 subwarp trade-off; §VII-C P:1743 "dynamic assignment or preprocessing with
+// approximate sorting").
+//
+// Per pair: validate, pick the precision path and the subwarp size G from a lane-step cost model
+// (the Q+G-1 ramp of SPEC S:262-279 plus a per-chunk-boundary spill term), then build a 64-bit
+// sort key  [bin:8][~Q:24][~tlen:32]  so that one CUB radix sort groups each bin contiguously,
+// longest queries first (LPT order for the persistent kernels' dynamic work queues), and places
+// pairs of near-identical shape next to each other (the int16x2 path packs neighbours).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+
+namespace saloba {
+
+// modelled lane-steps (one step = one 8x8 block on one lane) + spill cost, for group index g
+__host__ __device__ inline float group_cost(int Q, int strips, int g) {
+    const int G = 1 << g;
+    const int chunks = (strips + G - 1) / G;
+    const float steps = float(chunks) * float(Q + G - 1) * float(G);
+    const float spill = 0.5f * float(chunks - 1) * float(Q);  // write+read of 16 words per block column
+    return steps + spill;
+}
+
+__host__ __device__ inline int choose_gidx(int Q, int strips, int force_gidx, int min_gidx) {
+    if (force_gidx >= 0 && Q <= qmax_for_gidx(force_gidx)) return force_gidx;
+    int best = NGROUPS - 1;
+    float bc = group_cost(Q, strips, best);
+    for (int g = NGROUPS - 2; g >= min_gidx; --g) {
+        if (Q > qmax_for_gidx(g)) continue;
+        const float c = group_cost(Q, strips, g);
+        if (c < bc) {
+            bc = c;
+            best = g;
+        }
+    }
+    return best;
+}
+
+
+__global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
+    __shared__ int cnt[NBINS];
+    if (threadIdx.x < NBINS) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.n; k += int64_t(gridDim.x) * blockDim.x) {
+        const int n = a.q_len[k], m = a.t_len[k];
+        bool ok = n >= 1 && m >= 1 && n <= MAX_LEN && m <= MAX_LEN && n <= a.max_q_supported;
+        if (a.mode == SALOBA_EXTEND) {
+            const int h = a.h0[k];
+            ok = ok && h >= 1 && h <= MAX_H0;
+        }
+        int bin;
+        uint64_t key;
+        if (!ok) {
+            bin = BIN_SKIP;
+            a.score[k] = -1;
+            a.q_end[k] = -2;
+            a.t_end[k] = -2;
+            atomicMin(a.status, (unsigned long long)k);
+            key = (uint64_t(bin) << 56) | uint64_t(k);
+        } else {
+            const int Q = (n + 7) >> 3, strips = (m + 7) >> 3;
+            const int g = choose_gidx(Q, strips, a.force_gidx, 0);
+            const int path = PATH_I32;
+            bin = path * 8 + g;
+            if (a.keep_order)
+                key = (uint64_t(bin) << 56) | uint64_t(k);
+            else
+                key = (uint64_t(bin) << 56) | (uint64_t(0xFFFFFFu - uint32_t(min(Q, 0xFFFFFF))) << 32) |
+                      uint64_t(0xFFFFFFFFu - uint32_t(m));
+        }
+        a.keys[k] = key;
+        a.vals[k] = uint32_t(k);
+        atomicAdd(&cnt[bin], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < NBINS && cnt[threadIdx.x]) atomicAdd(a.bin_count + threadIdx.x, cnt[threadIdx.x]);
+}
+
+__global__ void bin_scan_kernel(const int32_t* count, int32_t* start) {
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int b = 0; b < NBINS; ++b) {
+            start[b] = acc;
+            acc += count[b];
+        }
+        start[NBINS] = acc;
+    }
+}
+
+size_t cub_sort_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, int(n > 0 ? n : 1), 0, 64);
+    return bytes;
+}
+
+cudaError_t run_classify_sort(const ClassifyArgs& ca, const SortKV& kv, int32_t* bin_start, int sms,
+                              cudaStream_t s) {
+    if (ca.n > 0) {
+        const int64_t g8 = int64_t(sms) * 8;
+        const int grid = int((ca.n + 255) / 256 < g8 ? (ca.n + 255) / 256 : g8);
+        classify_kernel<<<grid, 256, 0, s>>>(ca);
+        count_launches(1);
+        size_t tb = kv.cub_temp_bytes;
+        cudaError_t e = cub::DeviceRadixSort::SortPairs(kv.cub_temp, tb, kv.keys_in, kv.keys_out, kv.vals_in,
+                                                        kv.vals_out, int(ca.n), 0, 64, s);
+        if (e != cudaSuccess) return e;
+    }
+    bin_scan_kernel<<<1, 32, 0, s>>>(ca.bin_count, bin_start);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace saloba

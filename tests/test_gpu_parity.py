@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bar: bit-exact score, q_end and t_end (integer path).  Inputs are seeded: tiny
+exhaustive sets, randomized pairs with randomized schemes, every BASELINE config (full config 1;
+full-size configs 2-5 in the bench's launch configuration, compared on deterministic samples),
+and the edge cases (empty batch, 1-base pairs, N-rich pairs, invalid data, 2-bit packing).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+MODES = [oracle.LOCAL, oracle.EXTEND]
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import torch
+
+    import build_native
+
+    build_native.build_saloba()
+    import paper_2301_09310_b200 as sb
+
+    torch.cuda.init()
+    return sb
+
+
+def to_dev(batch):
+    import torch
+
+    d = "cuda"
+    return (torch.from_numpy(batch.q_ascii).to(d), torch.from_numpy(batch.q_off).to(d),
+            torch.from_numpy(batch.t_ascii).to(d), torch.from_numpy(batch.t_off).to(d),
+            torch.from_numpy(batch.h0).to(d))
+
+
+def gpu_align(sb, batch, scoring=None, mode=0, options=None, fmt=4):
+    import torch
+
+    scoring = scoring or sb.BWA_MEM
+    qa, qo, ta, to, h0 = to_dev(batch)
+    s, qe, te, st, qst, tst = sb.align(qa, qo, ta, to, h0 if mode == sb.EXTEND else None, scoring, mode, fmt,
+                                       options=options)
+    torch.cuda.synchronize()
+    return s.cpu().numpy(), qe.cpu().numpy(), te.cpu().numpy(), int(st.item()), int(qst.item()), int(tst.item())
+
+
+def oracle_align(batch, scoring, mode, threads=None):
+    s, qe, te, st, _ = oracle.align_batch(batch, scoring.match, scoring.mismatch, scoring.gap_open,
+                                          scoring.gap_extend, mode, threads=threads)
+    assert (st == 0).all()
+    return s, qe, te
+
+
+def assert_same(got, ref, batch, label):
+    s, qe, te = got[:3]
+    rs, rq, rt = ref
+    bad = np.nonzero((s != rs) | (qe != rq) | (te != rt))[0]
+    if len(bad):
+        k = int(bad[0])
+        q, t = batch.pair(k)
+        raise AssertionError(f"{label}: {len(bad)} mismatches; first k={k} gpu=({s[k]},{qe[k]},{te[k]}) "
+                             f"oracle=({rs[k]},{rq[k]},{rt[k]}) q={q[:80]!r} t={t[:80]!r} h0={batch.h0[k]}")
+
+
+# ---- A1 pack ---------------------------------------------------------------------------------
+def test_pack_spec_examples(sb):
+    import torch
+
+    b = synth.from_pairs([("ACGTN", "AAAAAAAA"), ("ACGTACGT", "acgtacgtu"), ("A" * 9, "N")])
+    qa, qo, ta, to, _ = to_dev(b)
+    w, wo, ln, st = sb.pack(qa, qo)
+    torch.cuda.synchronize()
+    w = w.cpu().numpy().view(np.uint32)
+    wo = wo.cpu().numpy()
+    assert int(st.item()) == -1
+    assert w[wo[0]] == 0xFFF43210  # S:50 "ACGTN" -> codes 0,1,2,3,4 then padding 15
+    assert w[wo[1]] == 0x32103210
+    assert w[wo[2]] == 0 and w[wo[2] + 1] == 0xFFFFFFF0  # 9 bases -> 2 words, 7 padding nibbles
+    assert ln.cpu().tolist() == [5, 8, 9]
+    w2, wo2, _, st2 = sb.pack(ta, to)
+    torch.cuda.synchronize()
+    w2 = w2.cpu().numpy().view(np.uint32)
+    wo2 = wo2.cpu().numpy()
+    assert w2[wo2[0]] == 0x00000000
+    assert w2[wo2[1]] == 0x32103210 and w2[wo2[1] + 1] == 0xFFFFFFF3  # lowercase + U -> T
+    assert w2[wo2[2]] == 0xFFFFFFF4
+
+
+def test_pack_random_vs_host_packer(sb):
+    import torch
+
+    rng = np.random.default_rng(0)
+    b = synth.random_pairs(3000, 1, 300, seed=1, alphabet=b"ACGTNacgtnUu")
+    qa, qo, _, _, _ = to_dev(b)
+    for fmt in (4,):
+        w, wo, ln, st = sb.pack(qa, qo, fmt)
+        torch.cuda.synchronize()
+        w = w.cpu().numpy().view(np.uint32)
+        wo = wo.cpu().numpy()
+        code = np.full(256, 255, np.uint8)
+        for ch, c in zip(b"ACGTUNacgtun", [0, 1, 2, 3, 3, 4, 0, 1, 2, 3, 3, 4]):
+            code[ch] = c
+        for k in rng.choice(b.n, 300, replace=False):
+            q = np.frombuffer(b.pair(int(k))[0], np.uint8)
+            cs = code[q]
+            nw = (len(cs) + 7) // 8
+            exp = np.full(nw * 8, 15, np.uint32)
+            exp[:len(cs)] = cs
+            expw = (exp.reshape(nw, 8) << (4 * np.arange(8, dtype=np.uint32))).sum(1).astype(np.uint32)
+            assert np.array_equal(w[wo[k]:wo[k] + nw], expw)
+    del rng
+
+
+def test_pack_invalid_base_reported(sb):
+    import torch
+
+    b = synth.from_pairs([("ACGT", "ACGT"), ("ACXT", "ACGT"), ("AC-T", "ACGT")])
+    qa, qo, _, _, _ = to_dev(b)
+    _, _, _, st = sb.pack(qa, qo)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 6  # first invalid byte: 'X' at global byte 4+2
+    b2 = synth.from_pairs([("ACGN", "ACGT")])
+    qa, qo, _, _, _ = to_dev(b2)
+    _, _, _, st = sb.pack(qa, qo, sb.PACK2)  # N is not representable in 2 bits
+    torch.cuda.synchronize()
+    assert int(st.item()) == 3
+
+
+# ---- A2-A4 DP parity -------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", MODES)
+def test_exhaustive_len_1_to_4(sb, mode):
+    """All 115,600 ordered pairs of ACGT strings of lengths 1..4 (SPEC acceptance 1)."""
+    strs = ["".join(p) for L in (1, 2, 3, 4) for p in itertools.product("ACGT", repeat=L)]
+    pairs = [(q, t) for q in strs for t in strs]
+    b = synth.from_pairs(pairs, np.full(len(pairs), 3, np.int32))
+    sc = sb.Scoring(1, -4, 2, 1)
+    assert_same(gpu_align(sb, b, sc, mode), oracle_align(b, sc, mode), b, f"exhaustive mode={mode}")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_randomized_schemes_1_to_512(sb, mode):
+    """>= 10,000 random pairs of 1-512 bp, schemes from SPEC acceptance 2's ranges."""
+    rng = np.random.default_rng(2023 + mode)
+    for r in range(12):
+        beta = int(rng.integers(1, 4))
+        sc = sb.Scoring(int(rng.integers(1, 5)), int(rng.integers(-6, 0)), int(rng.integers(beta, 9)), beta)
+        b = synth.random_pairs(900, 1, 512, seed=100 * r + mode, p_mut=0.1 if r % 2 else 0.0)
+        assert_same(gpu_align(sb, b, sc, mode), oracle_align(b, sc, mode), b, f"random r={r} {sc}")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_n_rich_pairs(sb, mode):
+    b = synth.random_pairs(2000, 1, 200, seed=5, alphabet=b"ACGTNN", p_mut=0.05)
+    sc = sb.BWA_MEM
+    assert_same(gpu_align(sb, b, sc, mode), oracle_align(b, sc, mode), b, "N-rich")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_config1_full(sb, mode):
+    b = synth.generate(1)
+    assert_same(gpu_align(sb, b, sb.BWA_MEM, mode), oracle_align(b, sb.BWA_MEM, mode), b, "config1")
+    bn = synth.generate(1, seed=11, p_n=0.005)  # parity-only N set (§8(d))
+    assert_same(gpu_align(sb, bn, sb.BWA_MEM, mode), oracle_align(bn, sb.BWA_MEM, mode), bn, "config1+N")
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8, 16, 32])
+def test_bit_identical_across_group_size(sb, G):
+    b = synth.random_pairs(1500, 1, 400, seed=77, p_mut=0.08)
+    ref = oracle_align(b, sb.BWA_MEM, oracle.LOCAL)
+    assert_same(gpu_align(sb, b, sb.BWA_MEM, 0, sb.Options(force_group=G)), ref, b, f"G={G}")
+    ref = oracle_align(b, sb.BWA_MEM, oracle.EXTEND)
+    assert_same(gpu_align(sb, b, sb.BWA_MEM, 1, sb.Options(force_group=G)), ref, b, f"G={G} extend")
+
+
+def test_order_and_path_invariance(sb):
+    b = synth.generate(3, 3000, seed=9)
+    base = gpu_align(sb, b, sb.BWA_MEM, 0)
+    for opt in (sb.Options(keep_order=1), sb.Options(force_path=1), sb.Options(force_path=2)):
+        got = gpu_align(sb, b, sb.BWA_MEM, 0, opt)
+        assert all(np.array_equal(x, y) for x, y in zip(base[:3], got[:3])), opt
+    # permuting the batch permutes the results
+    perm = np.random.default_rng(0).permutation(b.n)
+    bp = b.subset(perm)
+    got = gpu_align(sb, bp, sb.BWA_MEM, 0)
+    assert all(np.array_equal(x[perm], y) for x, y in zip(base[:3], got[:3]))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_pack2_path(sb, mode):
+    b = synth.random_pairs(1500, 1, 300, seed=31, p_mut=0.1)
+    ref = oracle_align(b, sb.BWA_MEM, mode)
+    assert_same(gpu_align(sb, b, sb.BWA_MEM, mode, fmt=2), ref, b, "pack2")
+
+
+def test_edge_cases(sb):
+    import torch
+
+    # empty batch
+    b = synth.from_pairs([])
+    qa, qo, ta, to, h0 = to_dev(b)
+    s, qe, te, st, _, _ = sb.align(qa, qo, ta, to)
+    torch.cuda.synchronize()
+    assert s.numel() == 0 and int(st.item()) == -1
+    # single bases, exact multiples of 8, one-off lengths
+    pairs = [("A", "A"), ("A", "C"), ("N", "N"), ("ACGTACGT", "ACGTACGT"), ("ACGTACGTA", "ACGTACGT"),
+             ("A" * 257, "A" * 255), ("ACGT" * 64, "TGCA" * 64)]
+    b = synth.from_pairs(pairs, np.array([1, 5, 9, 3, 2, 40, 7], np.int32))
+    for mode in MODES:
+        assert_same(gpu_align(sb, b, sb.BWA_MEM, mode), oracle_align(b, sb.BWA_MEM, mode), b, "edge")
+
+
+def test_invalid_pairs_reported(sb):
+    import torch
+
+    b = synth.from_pairs([("ACGT", "ACGT"), ("", "ACGT"), ("ACGT", ""), ("AC", "AC")],
+                         np.array([5, 5, 5, 0], np.int32))
+    qa, qo, ta, to, h0 = to_dev(b)
+    s, qe, te, st, _, _ = sb.align(qa, qo, ta, to)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 1
+    assert s.cpu().tolist() == [4, -1, -1, 2]
+    assert qe.cpu().tolist()[1:3] == [-2, -2]
+    s, qe, te, st, _, _ = sb.align(qa, qo, ta, to, h0, mode=sb.EXTEND)  # h0 = 0 is invalid for pair 3
+    torch.cuda.synchronize()
+    assert int(st.item()) == 1 and s.cpu().tolist() == [9, -1, -1, -1]
+
+
+def test_large_scores_int32_envelope(sb):
+    """match 1024 x 3000 bp identical reads: scores ~3e6 exceed int16, int32 path exact."""
+    rng = np.random.default_rng(4)
+    q = "".join(rng.choice(list("ACGT"), 3000))
+    t = q[:1000] + "GATTACA" + q[1000:]
+    b = synth.from_pairs([(q, t), (q, q)], np.array([100000, 7], np.int32))
+    sc = sb.Scoring(1024, -1024, 1024, 1)
+    for mode in MODES:
+        assert_same(gpu_align(sb, b, sc, mode), oracle_align(b, sc, mode), b, "big")
+
+
+# ---- full-size configs in the bench's launch configuration, sampled -----------------------------
+def _sample_check(sb, cfg, n=None, sample=3000, mode=0, seed=None):
+    b = synth.generate(cfg, n, seed=seed)
+    got = gpu_align(sb, b, sb.BWA_MEM, mode)
+    assert got[3] == -1
+    rng = np.random.default_rng(cfg)
+    idx = np.sort(rng.choice(b.n, min(sample, b.n), replace=False))
+    # include the longest pairs too (they exercise the most chunks / spill rows)
+    longest = np.argsort(b.qlen.astype(np.int64) * b.tlen)[-20:]
+    idx = np.unique(np.concatenate([idx, longest]))
+    sub = b.subset(idx)
+    ref = oracle_align(sub, sb.BWA_MEM, mode)
+    assert_same(tuple(x[idx] for x in got[:3]), ref, sub, f"config{cfg} sample")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_config2_full_size_sampled(sb, mode):
+    _sample_check(sb, 2, mode=mode)
+
+
+def test_config3_full_size_sampled(sb):
+    _sample_check(sb, 3, sample=2000)
+
+
+def test_config4_sampled(sb):
+    _sample_check(sb, 4, n=2000, sample=40)
+
+
+def test_config5_sampled(sb):
+    _sample_check(sb, 5, n=300_000, sample=3000)
+
+
+def test_host_entry_point_matches_device_path(sb):
+    b = synth.generate(3, 5000, seed=3)
+    dev = gpu_align(sb, b, sb.BWA_MEM, 1)
+    s, qe, te, st = sb.align_host(b, sb.BWA_MEM, sb.EXTEND)
+    assert st == -1
+    assert np.array_equal(s, dev[0]) and np.array_equal(qe, dev[1]) and np.array_equal(te, dev[2])
