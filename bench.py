@@ -247,6 +247,9 @@ def main():
 
     dp_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                  for _ in range(args.steps)]
+    for e_a, e_b in dp_events:  # torch creates the CUDA events lazily: record once so they exist
+        e_a.record(stream)
+        e_b.record(stream)
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)

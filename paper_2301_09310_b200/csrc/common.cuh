@@ -27,6 +27,7 @@ __host__ __device__ constexpr int qmax_for_gidx(int gidx) {
 constexpr int MAX_LEN = 1 << 20;   // S:151 overflow envelope for int32 cells
 constexpr int MAX_H0 = 1 << 29;
 constexpr int BLOCK_THREADS = 256;
+constexpr int I16_THREADS = 128;
 
 struct SortKV {
     uint64_t* keys_in;
@@ -38,6 +39,10 @@ struct SortKV {
 };
 
 struct ClassifyArgs {
+    const uint32_t* q_words;  // to detect N in queries (int16x2 path needs N-free queries)
+    const int64_t* q_word_off;
+    int fmt;
+    int match;
     const int32_t* q_len;
     const int32_t* t_len;
     const int32_t* h0;

@@ -1,0 +1,422 @@
+// dp_i16.cu — A3 fast path: int16x2 "pair-SIMD" wavefront DP, two passes, exact results.
+//
+// Same wavefront as dp_i32.cu (§IV-A: 8x8 blocks, a strip of 8 target rows
+// per lane, G lanes per chunk, Q + G - 1 steps per chunk, top rows passed lane-to-lane by
+// __shfl_up_sync, only chunk-bottom rows spilled), but every 32-bit register holds the same cell
+// of TWO pairs (low / high 16 bits), so each sm_100a DPX instruction (VIADDMNMX.S16x2,
+// VIMNMX.S16x2.RELU, VIMNMX3.S16x2, VIADD.16x2) advances two DP tables.  The scheduler sorts
+// pairs by shape, so the two halves of a work item have (near-)identical dimensions.
+//
+// Cell update (Eqs. 1-3), per register = 2 cells:
+//     f  = max(f_up - beta, ha_up)          VIADDMNMX   (ha = H - alpha, shared by E and F)
+//     e  = max(e_left - beta, ha_left)      VIADDMNMX
+//     s  = PRMT(table_A[row], table_B[row], selector[col])      substitution score (int8 -> int16)
+//     x  = max(h_diag + s, e)               VIADDMNMX   (LOCAL; EXTEND kills dead diagonals, below)
+//     h  = max(0, x, f)                     VIMNMX.RELU
+//     ha = h - alpha                        VIADD.16x2
+//     M  = max(M, h, h')                    VIMNMX3     (running maximum, 1 per 2 cells)
+//
+// Exact end coordinates without per-cell bookkeeping:
+//   pass 1 tracks only the running maximum, reduced per chunk; the first chunk that reaches the
+//   pair's maximum contains the tie-rule winner (rows grow with the chunk index).
+//   The top boundary of that chunk is the previous chunk's spilled bottom row, kept alive by a
+//   4-buffer rotation.  Pass 2 recomputes only that chunk from its checkpoint and finds the first
+//   cell (row-major) equal to the maximum.  Cost: ~1/chunks of pass 1.
+//
+// Exactness of the 16-bit lanes is guaranteed by routing (schedule.cu): all H, E, F stay in
+// [-alpha-beta, bound] with bound = match*min(m,n) (+h0, x2 in EXTEND) <= 32767 - match.
+// Padding: query columns past a half's length use selectors that sign-replicate a table byte,
+// giving S in {0, -1}; target rows past its length (and target N) use an all-mismatch table.
+// Padding cells are therefore never larger than a valid cell with a strictly smaller row (same
+// row: strictly smaller column), so they can neither raise the maximum nor win its tie-break.
+// Queries containing N are routed to the int32 path (a 4-entry table has no "never matches" slot).
+#include <climits>
+
+#include "common.cuh"
+
+namespace saloba {
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t vaddmax(uint32_t a, uint32_t b, uint32_t c) { return __viaddmax_s16x2(a, b, c); }
+__device__ __forceinline__ uint32_t vaddmin(uint32_t a, uint32_t b, uint32_t c) { return __viaddmin_s16x2(a, b, c); }
+__device__ __forceinline__ uint32_t vmaxrelu(uint32_t a, uint32_t b) { return __vimax_s16x2_relu(a, b); }
+__device__ __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) { return __vmaxs2(a, b); }
+__device__ __forceinline__ uint32_t vmax3(uint32_t a, uint32_t b, uint32_t c) { return __vimax3_s16x2(a, b, c); }
+__device__ __forceinline__ uint32_t vadd(uint32_t a, uint32_t b) { return __vadd2(a, b); }
+__device__ __forceinline__ uint32_t pack2(int lo, int hi) { return (uint32_t(lo) & 0xFFFFu) | (uint32_t(hi) << 16); }
+__device__ __forceinline__ int lo16(uint32_t v) { return int(int16_t(v & 0xFFFF)); }
+__device__ __forceinline__ int hi16(uint32_t v) { return int(int16_t(v >> 16)); }
+
+// 8 bases of block w of a packed sequence as nibbles; positions >= len read as 15 (padding)
+__device__ __forceinline__ uint32_t block_codes(const uint32_t* __restrict__ words, int w, int len, int fmt) {
+    const int valid = len - 8 * w;
+    if (valid <= 0) return 0xFFFFFFFFu;
+    uint32_t x = load_block8(words, w, fmt);
+    if (valid < 8) x |= 0xFFFFFFFFu << (4 * valid);
+    return x;
+}
+
+// substitution table of one target base t (nibble code) over query codes 0..3, as 4 int8 bytes
+__device__ __forceinline__ uint32_t row_table(uint32_t t, int ma, int mm) {
+    const uint32_t base = (uint32_t(mm) & 0xFFu) * 0x01010101u;
+    if (t >= 4) return base;  // N or padding: never matches
+    const uint32_t diff = (uint32_t(ma) ^ uint32_t(mm)) & 0xFFu;
+    return base ^ (diff << (8 * t));
+}
+
+// the 8 PRMT selectors of one query block for halves A (codes qa) and B (codes qb):
+// selector nibbles [a, a|8, b^4, (b^4)|8]; code 15 (padding) becomes a sign-replicating index.
+__device__ __forceinline__ void make_selectors(uint32_t qa, uint32_t qb, uint32_t (&sel)[8]) {
+    const uint32_t ae = qa & 0x0F0F0F0Fu, ao = (qa >> 4) & 0x0F0F0F0Fu;                     // cols 0,2,4,6 / 1,3,5,7
+    const uint32_t be = (qb & 0x0F0F0F0Fu) ^ 0x04040404u, bo = ((qb >> 4) & 0x0F0F0F0Fu) ^ 0x04040404u;
+    const uint32_t sae = ae | (ae << 4) | 0x80808080u, sao = ao | (ao << 4) | 0x80808080u;  // [x, x|8] per byte
+    const uint32_t sbe = be | (be << 4) | 0x80808080u, sbo = bo | (bo << 4) | 0x80808080u;
+    sel[0] = prmt(sae, sbe, 0x0040);
+    sel[1] = prmt(sao, sbo, 0x0040);
+    sel[2] = prmt(sae, sbe, 0x0051);
+    sel[3] = prmt(sao, sbo, 0x0051);
+    sel[4] = prmt(sae, sbe, 0x0062);
+    sel[5] = prmt(sao, sbo, 0x0062);
+    sel[6] = prmt(sae, sbe, 0x0073);
+    sel[7] = prmt(sao, sbo, 0x0073);
+}
+
+struct HalfInfo {
+    int n, m, h0, p;  // p < 0: dummy half
+};
+
+// One chunk of the wavefront for both halves.  PASS 1: returns the lane's running maximum.
+// PASS 2: searches for the first cell equal to `target` (per half) and returns hit rows/cols.
+// rowA0 / rowB0: first target row of lane 0 of this chunk in each half (they differ in pass 2).
+template <int G, int MODE, bool PASS2>
+__device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned mask, const int k, const int Q,
+                                              const HalfInfo& A, const HalfInfo& B,
+                                              const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
+                                              const uint32_t* __restrict__ twA, const uint32_t* __restrict__ twB,
+                                              const int rowA0, const int rowB0,
+                                              const uint32_t* rdHA, const uint32_t* rdFA,  // top rows (nullptr: boundary)
+                                              const uint32_t* rdHB, const uint32_t* rdFB,
+                                              uint32_t* wrH, uint32_t* wrF,  // bottom rows out (nullptr: none)
+                                              const uint32_t target, int (&hit)[4]) {
+    const int al = a.alpha, be = a.beta;
+    const uint32_t nbeta = pack2(-be, -be), nalpha = pack2(-al, -al);
+    const int rA = rowA0 + 8 * k, rB = rowB0 + 8 * k;  // my first row in each half
+    // row tables
+    uint32_t tabA[8], tabB[8];
+    {
+        const uint32_t ta = (rA < A.m) ? block_codes(twA, rA >> 3, A.m, a.fmt) : 0xFFFFFFFFu;
+        const uint32_t tb = (rB < B.m) ? block_codes(twB, rB >> 3, B.m, a.fmt) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            tabA[r] = row_table((ta >> (4 * r)) & 15u, a.match, a.mismatch);
+            tabB[r] = row_table((tb >> (4 * r)) & 15u, a.match, a.mismatch);
+        }
+    }
+    // left boundary H(i,-1), E(i,-1) = 0, corner H(r0-1,-1)
+    // Hl[r] = H(r, c-1); En[r] = E(r, c) = max(E(r, c-1) - beta, H(r, c-1) - alpha), kept one column
+    // ahead so that H - alpha is consumed immediately (no register for it).
+    uint32_t Hl[8], En[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const int ha = MODE ? max(0, A.h0 - al - be * (rA + r)) : 0;
+        const int hb = MODE ? max(0, B.h0 - al - be * (rB + r)) : 0;
+        Hl[r] = pack2(ha, hb);
+        // E(i,0) = max(H(i,-1) - alpha, E(i,-1) - beta); taking E(i,-1) as "no gap" changes only
+        // non-positive E values, which never reach H = max(0, ...) (clamp neutrality)
+        En[r] = vadd(Hl[r], nalpha);
+    }
+    uint32_t corner;
+    {
+        const int ca = MODE ? (rA == 0 ? A.h0 : max(0, A.h0 - al - be * (rA - 1))) : 0;
+        const int cb = MODE ? (rB == 0 ? B.h0 : max(0, B.h0 - al - be * (rB - 1))) : 0;
+        corner = pack2(ca, cb);
+    }
+    uint32_t M0 = 0, M1 = 0, M2 = 0, M3 = 0;
+    uint32_t botH[8], botF[8];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) botH[x] = botF[x] = 0;
+    const bool lane_rows = (rA < A.m) || (rB < B.m);
+    const int steps = Q + G - 1;
+    for (int s = 0; s < steps; ++s) {
+        const int w = s - k;
+        uint32_t topH[8], topF[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+            topH[x] = __shfl_up_sync(mask, botH[x], 1, G);
+            topF[x] = __shfl_up_sync(mask, botF[x], 1, G);
+        }
+        if (k == 0 && w < Q) {
+            // top row of the chunk: spilled row of the previous chunk, or the table boundary
+            uint32_t bhA[8], bfA[8], bhB[8], bfB[8];
+            if (rdHA) {
+                const uint4* ph = reinterpret_cast<const uint4*>(rdHA + 8 * w);
+                const uint4* pf = reinterpret_cast<const uint4*>(rdFA + 8 * w);
+                uint4 h0v = ph[0], h1v = ph[1], f0v = pf[0], f1v = pf[1];
+                bhA[0] = h0v.x; bhA[1] = h0v.y; bhA[2] = h0v.z; bhA[3] = h0v.w;
+                bhA[4] = h1v.x; bhA[5] = h1v.y; bhA[6] = h1v.z; bhA[7] = h1v.w;
+                bfA[0] = f0v.x; bfA[1] = f0v.y; bfA[2] = f0v.z; bfA[3] = f0v.w;
+                bfA[4] = f1v.x; bfA[5] = f1v.y; bfA[6] = f1v.z; bfA[7] = f1v.w;
+            } else {
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    const int j = 8 * w + x;
+                    bhA[x] = pack2(MODE ? max(0, A.h0 - al - be * j) : 0, MODE ? max(0, B.h0 - al - be * j) : 0);
+                    bfA[x] = pack2(-al - be, -al - be);
+                }
+            }
+            if (PASS2 && rdHB != rdHA) {
+                if (rdHB) {
+                    const uint4* ph = reinterpret_cast<const uint4*>(rdHB + 8 * w);
+                    const uint4* pf = reinterpret_cast<const uint4*>(rdFB + 8 * w);
+                    uint4 h0v = ph[0], h1v = ph[1], f0v = pf[0], f1v = pf[1];
+                    bhB[0] = h0v.x; bhB[1] = h0v.y; bhB[2] = h0v.z; bhB[3] = h0v.w;
+                    bhB[4] = h1v.x; bhB[5] = h1v.y; bhB[6] = h1v.z; bhB[7] = h1v.w;
+                    bfB[0] = f0v.x; bfB[1] = f0v.y; bfB[2] = f0v.z; bfB[3] = f0v.w;
+                    bfB[4] = f1v.x; bfB[5] = f1v.y; bfB[6] = f1v.z; bfB[7] = f1v.w;
+                } else {
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        const int j = 8 * w + x;
+                        bhB[x] = pack2(MODE ? max(0, A.h0 - al - be * j) : 0, MODE ? max(0, B.h0 - al - be * j) : 0);
+                        bfB[x] = pack2(-al - be, -al - be);
+                    }
+                }
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {  // low half from A's source, high half from B's
+                    topH[x] = prmt(bhA[x], bhB[x], 0x7610);
+                    topF[x] = prmt(bfA[x], bfB[x], 0x7610);
+                }
+            } else {
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    topH[x] = bhA[x];
+                    topF[x] = bfA[x];
+                }
+            }
+        }
+        if (w >= 0 && w < Q && lane_rows) {
+            uint32_t sel[8];
+            make_selectors(block_codes(qwA, w, A.n, a.fmt), block_codes(qwB, w, B.n, a.fmt), sel);
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                uint32_t hup = topH[x], fup = topF[x];
+                uint32_t haup = vadd(hup, nalpha);
+                uint32_t hdiag = (x == 0) ? corner : topH[x - 1];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const uint32_t f = vaddmax(fup, nbeta, haup);
+                    const uint32_t e = En[r];
+                    const uint32_t sc = prmt(tabA[r], tabB[r], sel[x]);
+                    uint32_t xx;
+                    if (MODE) {
+                        // dead-zero (EXTEND): D = hdiag + s if hdiag > 0 else <= 0.
+                        // min(hdiag + s, 2^k * hdiag) with 2^k >= match + 1 (routing bound covers it)
+                        uint32_t kd = vadd(hdiag, hdiag);
+                        for (int q = 2; q < a.match + 1; q <<= 1) kd = vadd(kd, kd);
+                        xx = vmax(vaddmin(hdiag, sc, kd), e);
+                    } else {
+                        xx = vaddmax(hdiag, sc, e);
+                    }
+                    const uint32_t h = vmaxrelu(xx, f);
+                    const uint32_t ha = vadd(h, nalpha);
+                    hdiag = Hl[r];
+                    Hl[r] = h;
+                    En[r] = vaddmax(e, nbeta, ha);
+                    hup = h;
+                    haup = ha;
+                    fup = f;
+                    if (!PASS2) {
+                        if (r == 1) M0 = vmax3(M0, Hl[0], Hl[1]);
+                        if (r == 3) M1 = vmax3(M1, Hl[2], Hl[3]);
+                        if (r == 5) M2 = vmax3(M2, Hl[4], Hl[5]);
+                        if (r == 7) M3 = vmax3(M3, Hl[6], Hl[7]);
+                    }
+                }
+                botH[x] = hup;
+                botF[x] = fup;
+                if (PASS2) {
+                    // column maximum; a cell can only equal `target` (the pair maximum) if it is >= it
+                    const uint32_t cm = vmax3(vmax3(Hl[0], Hl[1], Hl[2]), vmax3(Hl[3], Hl[4], Hl[5]), vmax(Hl[6], Hl[7]));
+                    const bool hitA = lo16(cm) >= lo16(target), hitB = hi16(cm) >= hi16(target);
+                    if (hitA || hitB) {
+                        const int col = 8 * w + x;
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            if (hitA && lo16(Hl[r]) == lo16(target) && (rA + r < hit[0] || (rA + r == hit[0] && col < hit[1]))) {
+                                hit[0] = rA + r;
+                                hit[1] = col;
+                            }
+                            if (hitB && hi16(Hl[r]) == hi16(target) && (rB + r < hit[2] || (rB + r == hit[2] && col < hit[3]))) {
+                                hit[2] = rB + r;
+                                hit[3] = col;
+                            }
+                        }
+                    }
+                }
+            }
+            corner = topH[7];
+            if (wrH && k == G - 1) {
+                uint4* ph = reinterpret_cast<uint4*>(wrH + 8 * w);
+                uint4* pf = reinterpret_cast<uint4*>(wrF + 8 * w);
+                ph[0] = make_uint4(botH[0], botH[1], botH[2], botH[3]);
+                ph[1] = make_uint4(botH[4], botH[5], botH[6], botH[7]);
+                pf[0] = make_uint4(botF[0], botF[1], botF[2], botF[3]);
+                pf[1] = make_uint4(botF[4], botF[5], botF[6], botF[7]);
+            }
+        }
+    }
+    return vmax(vmax(M0, M1), vmax(M2, M3));
+}
+
+template <int G, int MODE>
+__global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bin) {
+    const int lane = threadIdx.x & 31;
+    const int k = lane & (G - 1);
+    const int sub_base = lane & ~(G - 1);
+    const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << sub_base);
+    const int64_t slot = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+    const int64_t S = a.spill_stride;
+    uint32_t* const spill = reinterpret_cast<uint32_t*>(a.spill) + slot * 8 * S;  // 4 buffers x (H, F)
+
+    const int start = a.bin_start[bin];
+    const int cnt = a.bin_start[bin + 1] - start;
+    const int items = (cnt + 1) >> 1;
+
+    for (;;) {
+        int item = 0;
+        if (k == 0) item = atomicAdd(a.bin_counter + bin, 1);
+        item = __shfl_sync(mask, item, 0, G);
+        if (item >= items) break;
+        HalfInfo A, B;
+        A.p = int(a.perm[start + 2 * item]);
+        B.p = (2 * item + 1 < cnt) ? int(a.perm[start + 2 * item + 1]) : -1;
+        A.n = a.q_len[A.p];
+        A.m = a.t_len[A.p];
+        A.h0 = MODE ? a.h0[A.p] : 0;
+        B.n = B.p >= 0 ? a.q_len[B.p] : 0;
+        B.m = B.p >= 0 ? a.t_len[B.p] : 0;
+        B.h0 = (MODE && B.p >= 0) ? a.h0[B.p] : 0;
+        const uint32_t* qwA = a.q_words + a.q_word_off[A.p];
+        const uint32_t* twA = a.t_words + a.t_word_off[A.p];
+        const uint32_t* qwB = B.p >= 0 ? a.q_words + a.q_word_off[B.p] : qwA;
+        const uint32_t* twB = B.p >= 0 ? a.t_words + a.t_word_off[B.p] : twA;
+        const int Q = (max(A.n, B.n) + 7) >> 3;
+        const int chunksA = (((A.m + 7) >> 3) + G - 1) / G, chunksB = (((B.m + 7) >> 3) + G - 1) / G;
+        const int chunks = max(chunksA, chunksB);
+
+        // pass 1 -------------------------------------------------------------------------------
+        const int floorA = MODE ? A.h0 : 0, floorB = MODE ? B.h0 : 0;
+        int bestA = floorA, bestB = floorB;   // running maxima (strict improvement records chunk)
+        int ckA = -1, ckB = -1;               // chunk holding the first maximum (-1: none above floor)
+        int bufA = -1, bufB = -1;             // buffer holding that chunk's top row (-1: boundary)
+        int rd = -1, wr = 0;
+        for (int c = 0; c < chunks; ++c) {
+            const bool last = (c + 1 == chunks);
+            const uint32_t* rdH = rd >= 0 ? spill + (2 * rd) * S : nullptr;
+            const uint32_t* rdF = rd >= 0 ? spill + (2 * rd + 1) * S : nullptr;
+            uint32_t* wrH = last ? nullptr : spill + (2 * wr) * S;
+            uint32_t* wrF = last ? nullptr : spill + (2 * wr + 1) * S;
+            int dummy[4];
+            uint32_t m = run_chunk<G, MODE, false>(a, mask, k, Q, A, B, qwA, qwB, twA, twB, c * 8 * G, c * 8 * G,
+                                                   rdH, rdF, rdH, rdF, wrH, wrF, 0u, dummy);
+#pragma unroll
+            for (int off = 1; off < G; off <<= 1) m = vmax(m, __shfl_xor_sync(mask, m, off, G));
+            if (lo16(m) > bestA) {
+                bestA = lo16(m);
+                ckA = c;
+                bufA = rd;
+            }
+            if (hi16(m) > bestB) {
+                bestB = hi16(m);
+                ckB = c;
+                bufB = rd;
+            }
+            __syncwarp(mask);
+            if (!last) {
+                rd = wr;
+                // next write buffer: not the new read buffer nor a live checkpoint
+                int nw = 0;
+                while (nw == rd || nw == bufA || nw == bufB) ++nw;
+                wr = nw;
+            }
+        }
+        // pass 2 -------------------------------------------------------------------------------
+        int hit[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
+        if (ckA >= 0 || ckB >= 0) {
+            const int cA = ckA >= 0 ? ckA : ckB, cB = ckB >= 0 ? ckB : ckA;
+            const int bA = ckA >= 0 ? bufA : bufB, bB = ckB >= 0 ? bufB : bufA;
+            const uint32_t* hA = bA >= 0 ? spill + (2 * bA) * S : nullptr;
+            const uint32_t* fA = bA >= 0 ? spill + (2 * bA + 1) * S : nullptr;
+            const uint32_t* hB = bB >= 0 ? spill + (2 * bB) * S : nullptr;
+            const uint32_t* fB = bB >= 0 ? spill + (2 * bB + 1) * S : nullptr;
+            const uint32_t target = pack2(ckA >= 0 ? bestA : 0x7FFF, ckB >= 0 ? bestB : 0x7FFF);
+            run_chunk<G, MODE, true>(a, mask, k, Q, A, B, qwA, qwB, twA, twB, cA * 8 * G, cB * 8 * G, hA, fA,
+                                     hB, fB, nullptr, nullptr, target, hit);
+            // first hit in row-major order across the subwarp (rows grow with the lane index)
+#pragma unroll
+            for (int off = 1; off < G; off <<= 1) {
+                const int r0 = __shfl_xor_sync(mask, hit[0], off, G), c0 = __shfl_xor_sync(mask, hit[1], off, G);
+                const int r1 = __shfl_xor_sync(mask, hit[2], off, G), c1 = __shfl_xor_sync(mask, hit[3], off, G);
+                if (r0 < hit[0] || (r0 == hit[0] && c0 < hit[1])) {
+                    hit[0] = r0;
+                    hit[1] = c0;
+                }
+                if (r1 < hit[2] || (r1 == hit[2] && c1 < hit[3])) {
+                    hit[2] = r1;
+                    hit[3] = c1;
+                }
+            }
+        }
+        __syncwarp(mask);
+        if (k == 0) {
+            const int z = MODE ? -1 : 0;
+            a.score[A.p] = bestA;
+            a.t_end[A.p] = ckA >= 0 ? (hit[0] == INT_MAX ? -3 : hit[0]) : z;
+            a.q_end[A.p] = ckA >= 0 ? (hit[1] == INT_MAX ? -3 : hit[1]) : z;
+            if (B.p >= 0) {
+                a.score[B.p] = bestB;
+                a.t_end[B.p] = ckB >= 0 ? (hit[2] == INT_MAX ? -3 : hit[2]) : z;
+                a.q_end[B.p] = ckB >= 0 ? (hit[3] == INT_MAX ? -3 : hit[3]) : z;
+            }
+        }
+    }
+}
+
+template <int MODE>
+static void launch_i16_mode(int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s) {
+    switch (gidx) {
+    case 0: dp_i16_kernel<1, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
+    case 1: dp_i16_kernel<2, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
+    case 2: dp_i16_kernel<4, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
+    case 3: dp_i16_kernel<8, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
+    case 4: dp_i16_kernel<16, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
+    default: dp_i16_kernel<32, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
+    }
+}
+
+void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s) {
+    if (mode == SALOBA_EXTEND) launch_i16_mode<1>(gidx, grid, a, bin, s);
+    else launch_i16_mode<0>(gidx, grid, a, bin, s);
+    count_launches(1);
+}
+
+template <int MODE>
+static const void* kptr16_mode(int gidx) {
+    switch (gidx) {
+    case 0: return (const void*)dp_i16_kernel<1, MODE>;
+    case 1: return (const void*)dp_i16_kernel<2, MODE>;
+    case 2: return (const void*)dp_i16_kernel<4, MODE>;
+    case 3: return (const void*)dp_i16_kernel<8, MODE>;
+    case 4: return (const void*)dp_i16_kernel<16, MODE>;
+    default: return (const void*)dp_i16_kernel<32, MODE>;
+    }
+}
+const void* dp_i16_kernel_ptr(int mode, int gidx) {
+    return mode == SALOBA_EXTEND ? kptr16_mode<1>(gidx) : kptr16_mode<0>(gidx);
+}
+
+}  // namespace saloba

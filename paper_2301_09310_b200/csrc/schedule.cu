@@ -38,6 +38,29 @@ __host__ __device__ inline int choose_gidx(int Q, int strips, int force_gidx, in
 }
 
 
+// int16x2 routing: bit-exact iff every H, E, F fits in int16 — all values lie in
+// [-alpha-2beta, B] with B = match*min(m,n) (LOCAL) or h0 + match*min(m,n) (EXTEND); EXTEND also
+// forms 2^k*H (2^k >= match+1) for its dead-zero rule.  Queries must be N-free (4-entry tables).
+__device__ inline bool i16_eligible(const ClassifyArgs& a, int64_t k, int n, int m) {
+    const long long mn = n < m ? n : m;
+    long long B = (long long)a.match * mn;
+    long long lam = 1;
+    if (a.mode == SALOBA_EXTEND) {
+        B += a.h0[k];
+        lam = 2;
+        while (lam < a.match + 1) lam <<= 1;
+    }
+    if (lam * B + a.match > 32767) return false;
+    if (a.fmt == SALOBA_PACK2) return true;  // 2-bit sequences cannot hold N
+    const uint32_t* w = a.q_words + a.q_word_off[k];
+    const int nw = (n + 7) >> 3;
+    for (int i = 0; i < nw; ++i) {
+        const uint32_t v = __ldg(w + i) ^ 0x44444444u;  // nibble == 4 (N) -> zero nibble
+        if ((v - 0x11111111u) & ~v & 0x88888888u) return false;
+    }
+    return true;
+}
+
 __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
     __shared__ int cnt[NBINS];
     if (threadIdx.x < NBINS) cnt[threadIdx.x] = 0;
@@ -60,8 +83,8 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
             key = (uint64_t(bin) << 56) | uint64_t(k);
         } else {
             const int Q = (n + 7) >> 3, strips = (m + 7) >> 3;
+            const int path = (a.force_path != 1 && i16_eligible(a, k, n, m)) ? PATH_I16 : PATH_I32;
             const int g = choose_gidx(Q, strips, a.force_gidx, 0);
-            const int path = PATH_I32;
             bin = path * 8 + g;
             if (a.keep_order)
                 key = (uint64_t(bin) << 56) | uint64_t(k);
