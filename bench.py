@@ -35,8 +35,11 @@ WORKLOADS = {
     4: "config4: 100k long-read pairs, 1-10 kbp, ~15% errors",
     5: "config5: 10M length-skewed pairs (Fig. 3 histograms + long tails)",
 }
-# algorithmic int lane-ops per cell: 5 recurrence + 1 substitution + 1 running max
-OPS_PER_CELL = {"int32": 7.0, "int16x2": 3.5}
+# Minimal ALU-pipe instructions per cell.  Per register the update needs 3 max-type
+# ops (E, F, H), the substitution lookup (PRMT) and half a running-max op: 4.5 ALU-only
+# instructions (max/min/PRMT have no FMA-pipe form on sm_100a; the two adds go to the FMA pipe).
+# int16x2 registers carry 2 cells -> 2.25 ALU ops per cell; int32 -> 4.5.
+OPS_PER_CELL = {"int32": 4.5, "int16x2": 2.25}
 
 
 def parse():
@@ -135,7 +138,7 @@ def load_intpipe():
     try:
         with open(path) as f:
             d = json.load(f)
-        return float(d["alu_lane_ops_per_clk_per_sm"]), "measured (profiles/intpipe_b200.json)"
+        return float(d["alu_lane_ops_per_clk_per_sm"]), "measured ALU pipe rate (profiles/intpipe_b200.json)"
     except Exception:
         return 64.0, "guide: alu pipe rt_SMSP=2 -> 16 lanes/clk/SMSP x 4 (B300_MICROARCH.md)"
 
@@ -232,8 +235,10 @@ def main():
     if world > 1:
         gather_buf = [torch.empty((3, n), dtype=torch.int32, device=dev) for _ in range(world)] if rank == 0 else None
 
+    bins = torch.zeros(16, dtype=torch.int32, device=dev)
+
     def step(dp_ev=None):
-        o = sb.Options(args.force_group, args.force_path, args.keep_order, dp_ev) if dp_ev else None
+        o = sb.Options(args.force_group, args.force_path, args.keep_order, dp_ev, bins) if dp_ev else None
         s, qe, te = al.run(qa, qo, ta, to, h0, options=o)
         if world > 1:  # A5: results gathered to rank 0 (the only collective; none inside the DP)
             dist.gather(al.out[:, :n], gather_buf if rank == 0 else None, dst=0)
@@ -309,15 +314,19 @@ def main():
     p_int, p_src = load_intpipe()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_mhz = csum["sm_mhz"] or 1965.0
-    path = "int32"  # round 1: every pair takes the int32 exact path
+    bc = bins.cpu().tolist()
+    n16, n32 = sum(bc[8:15]), sum(bc[0:8])
+    path = "int16x2" if n16 >= n32 else "int32"
     peak = sms * f_mhz * 1e6 * p_int / OPS_PER_CELL[path] / 1e9
     achieved = cells_rank / (dp_ms_avg * 1e-3) / 1e9
     roof = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GCUPS",
             "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": "dp_i32_kernel (all G bins of one call, CUDA events on the launching stream)",
+            "kernel": ("dp_i16_kernel" if path == "int16x2" else "dp_i32_kernel") +
+                      " (all bins of one call, CUDA events on the launching stream)",
+            "bins": {f"{'i16' if b >= 8 else 'i32'}_G{1 << (b % 8)}": c for b, c in enumerate(bc) if c and b != 15},
             "dp_share_of_step": round(dp_ms_avg / ms_per_step, 3),
             "peak_derivation": f"{sms} SMs x {f_mhz:.0f} MHz (median under load) x {p_int:.0f} int lane-ops/clk/SM "
-                               f"[{p_src}] / {OPS_PER_CELL[path]} ops per cell ({path} path)"}
+                               f"[{p_src}] / {OPS_PER_CELL[path]} ALU ops per cell ({path} path)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(batch, mode, args.cpu_seconds)

@@ -84,7 +84,9 @@ typedef struct {
     void* ev_dp_begin;    /* optional cudaEvent_t recorded on `stream` right before the first DP
                              kernel launch of the call (after packing/scheduling), for profiling */
     void* ev_dp_end;      /* optional cudaEvent_t recorded on `stream` after the last DP kernel   */
-    int32_t reserved[4];
+    int32_t* bin_counts;  /* optional [dev] int32[16]: pairs per scheduler bin of this call, bin =
+                             path*8 + log2(G), path 0 = int32 exact, 1 = int16x2; bin 15 = invalid */
+    int32_t reserved[2];
 } saloba_options;
 
 /* ---- A1: packing --------------------------------------------------------------------------- */

@@ -46,7 +46,7 @@ class _Scoring(ctypes.Structure):
 class _Options(ctypes.Structure):
     _fields_ = [("force_group", ctypes.c_int32), ("force_path", ctypes.c_int32), ("keep_order", ctypes.c_int32),
                 ("reserved0", ctypes.c_int32), ("ev_dp_begin", ctypes.c_void_p), ("ev_dp_end", ctypes.c_void_p),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("bin_counts", ctypes.c_void_p), ("reserved", ctypes.c_int32 * 2)]
 
 
 @dataclass(frozen=True)
@@ -72,12 +72,15 @@ class Options:
     force_path: int = 0  # 0 auto, 1 int32 exact, 2 prefer int16x2
     keep_order: int = 0  # 1 = no length sort
     dp_events: tuple | None = None  # (torch.cuda.Event, torch.cuda.Event) bracketing the DP kernels
+    bin_counts: torch.Tensor | None = None  # cuda int32[16] <- pairs per bin (path*8 + log2 G)
 
     def _c(self) -> _Options:
         o = _Options(self.force_group, self.force_path, self.keep_order, 0)
         if self.dp_events is not None:
             o.ev_dp_begin = ctypes.c_void_p(self.dp_events[0].cuda_event)
             o.ev_dp_end = ctypes.c_void_p(self.dp_events[1].cuda_event)
+        if self.bin_counts is not None:
+            o.bin_counts = ctypes.c_void_p(self.bin_counts.data_ptr())
         return o
 
 

@@ -218,6 +218,7 @@ SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word
         a.score = score; a.q_end = q_end; a.t_end = t_end;
         a.perm = kv.vals_out; a.bin_start = bin_start; a.bin_counter = bin_counter;
         a.spill = reinterpret_cast<int32_t*>(ws + L.spill);
+        if (o.bin_counts) cudaMemcpyAsync(o.bin_counts, bin_count, NBINS * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
         if (o.ev_dp_begin) cudaEventRecord((cudaEvent_t)o.ev_dp_begin, s);
         for (int path = PATH_I16; path >= PATH_I32; --path)
             for (int g = NGROUPS - 1; g >= 0; --g) {

@@ -4,16 +4,19 @@
 // per lane, G lanes per chunk, Q + G - 1 steps per chunk, top rows passed lane-to-lane by
 // __shfl_up_sync, only chunk-bottom rows spilled), but every 32-bit register holds the same cell
 // of TWO pairs (low / high 16 bits), so each sm_100a DPX instruction (VIADDMNMX.S16x2,
-// VIMNMX.S16x2.RELU, VIMNMX3.S16x2, VIADD.16x2) advances two DP tables.  The scheduler sorts
+// VIMNMX3.S16x2(.RELU), VIADD.16x2) advances two DP tables.  Measured on B200 (tools/intpipe.cu,
+// profiles/intpipe_b200.json): VIADDMNMX / VIMNMX3 / PRMT issue on the ALU pipe, VIADD.16x2 and
+// IMAD on the FMA-heavy pipe, each 64 lanes/clk/SM; the update below puts 4.5 of its 6.5
+// instructions per register on the ALU pipe and 2 on the FMA pipe.  The scheduler sorts
 // pairs by shape, so the two halves of a work item have (near-)identical dimensions.
 //
 // Cell update (Eqs. 1-3), per register = 2 cells:
 //     f  = max(f_up - beta, ha_up)          VIADDMNMX   (ha = H - alpha, shared by E and F)
-//     e  = max(e_left - beta, ha_left)      VIADDMNMX
+//     e  = max(e_left - beta, ha_left)      VIADDMNMX   (computed one column ahead)
 //     s  = PRMT(table_A[row], table_B[row], selector[col])      substitution score (int8 -> int16)
-//     x  = max(h_diag + s, e)               VIADDMNMX   (LOCAL; EXTEND kills dead diagonals, below)
-//     h  = max(0, x, f)                     VIMNMX.RELU
-//     ha = h - alpha                        VIADD.16x2
+//     d  = h_diag + s                       VIADD.16x2  (FMA pipe; EXTEND: min(d, lambda*h_diag))
+//     h  = max(0, d, e, f)                  VIMNMX3.RELU
+//     ha = h - alpha                        VIADD.16x2  (FMA pipe)
 //     M  = max(M, h, h')                    VIMNMX3     (running maximum, 1 per 2 cells)
 //
 // Exact end coordinates without per-cell bookkeeping:
@@ -46,6 +49,7 @@ __device__ __forceinline__ uint32_t vaddmin(uint32_t a, uint32_t b, uint32_t c) 
 __device__ __forceinline__ uint32_t vmaxrelu(uint32_t a, uint32_t b) { return __vimax_s16x2_relu(a, b); }
 __device__ __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) { return __vmaxs2(a, b); }
 __device__ __forceinline__ uint32_t vmax3(uint32_t a, uint32_t b, uint32_t c) { return __vimax3_s16x2(a, b, c); }
+__device__ __forceinline__ uint32_t vmax3relu(uint32_t a, uint32_t b, uint32_t c) { return __vimax3_s16x2_relu(a, b, c); }
 __device__ __forceinline__ uint32_t vadd(uint32_t a, uint32_t b) { return __vadd2(a, b); }
 __device__ __forceinline__ uint32_t pack2(int lo, int hi) { return (uint32_t(lo) & 0xFFFFu) | (uint32_t(hi) << 16); }
 __device__ __forceinline__ int lo16(uint32_t v) { return int(int16_t(v & 0xFFFF)); }
@@ -104,6 +108,8 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                                               const uint32_t target, int (&hit)[4]) {
     const int al = a.alpha, be = a.beta;
     const uint32_t nbeta = pack2(-be, -be), nalpha = pack2(-al, -al);
+    uint32_t lam = 2;
+    while (int(lam) < a.match + 1) lam <<= 1;
     const int rA = rowA0 + 8 * k, rB = rowB0 + 8 * k;  // my first row in each half
     // row tables
     uint32_t tabA[8], tabB[8];
@@ -211,17 +217,16 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                     const uint32_t f = vaddmax(fup, nbeta, haup);
                     const uint32_t e = En[r];
                     const uint32_t sc = prmt(tabA[r], tabB[r], sel[x]);
-                    uint32_t xx;
+                    uint32_t h;
                     if (MODE) {
-                        // dead-zero (EXTEND): D = hdiag + s if hdiag > 0 else <= 0.
-                        // min(hdiag + s, 2^k * hdiag) with 2^k >= match + 1 (routing bound covers it)
-                        uint32_t kd = vadd(hdiag, hdiag);
-                        for (int q = 2; q < a.match + 1; q <<= 1) kd = vadd(kd, kd);
-                        xx = vmax(vaddmin(hdiag, sc, kd), e);
+                        // dead-zero (EXTEND): D = hdiag + s if hdiag > 0, else <= 0:
+                        // D = min(hdiag + s, lambda * hdiag), lambda = 2^k >= match + 1.  hdiag >= 0 and
+                        // lambda * hdiag <= 32767 (routing bound), so one 32-bit IMAD scales both halves.
+                        const uint32_t kd = hdiag * lam;
+                        h = vmax3relu(vaddmin(hdiag, sc, kd), e, f);
                     } else {
-                        xx = vaddmax(hdiag, sc, e);
+                        h = vmax3relu(vadd(hdiag, sc), e, f);  // D on the FMA pipe, one ALU max
                     }
-                    const uint32_t h = vmaxrelu(xx, f);
                     const uint32_t ha = vadd(h, nalpha);
                     hdiag = Hl[r];
                     Hl[r] = h;
