@@ -20,7 +20,7 @@ void launch_status_final(int64_t* st, cudaStream_t s);
 void launch_dp_i32(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s);
 const void* dp_i32_kernel_ptr(int mode, int gidx);
 void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s);
-const void* dp_i16_kernel_ptr(int mode, int gidx);
+const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt);
 void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n, int64_t base, int fmt,
                        uint32_t* words, int64_t* word_off, int32_t* lens, int64_t* status, cudaStream_t s);
 
@@ -51,7 +51,7 @@ static const DevInfo* dev_info(int device) {
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i32_kernel_ptr(mode, g), BLOCK_THREADS, 0);
                 d.blocks_i32[mode][g] = std::max(1, nb);
                 nb = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i16_kernel_ptr(mode, g), I16_THREADS, 0);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i16_kernel_ptr(mode, g, SALOBA_PACK4), I16_THREADS, 0);
                 d.blocks_i16[mode][g] = std::max(1, nb);
             }
         cudaSetDevice(prev);
@@ -78,8 +78,8 @@ static int grid_for(const DevInfo* d, int mode, int path, int g) {
     return d->sms * (path == PATH_I16 ? d->blocks_i16[mode][g] : d->blocks_i32[mode][g]);
 }
 static int threads_for(int path) { return path == PATH_I16 ? I16_THREADS : BLOCK_THREADS; }
-// spill rows per subwarp slot: int32 path 2 buffers x (H, F); int16x2 path 4 buffers x (H, F)
-static int rows_for(int path) { return path == PATH_I16 ? 8 : 4; }
+// spill rows per subwarp slot: int32 path 2 buffers x (H, F); int16x2 path 4 buffers x (H, F) + selectors
+static int rows_for(int path) { return path == PATH_I16 ? 9 : 4; }
 
 // bytes of spill pool the bin (mode, path, g) needs when the longest query has Qmax blocks
 static size_t spill_need(const DevInfo* d, int mode, int path, int g, int64_t Qmax) {

@@ -56,10 +56,11 @@ __device__ __forceinline__ int lo16(uint32_t v) { return int(int16_t(v & 0xFFFF)
 __device__ __forceinline__ int hi16(uint32_t v) { return int(int16_t(v >> 16)); }
 
 // 8 bases of block w of a packed sequence as nibbles; positions >= len read as 15 (padding)
-__device__ __forceinline__ uint32_t block_codes(const uint32_t* __restrict__ words, int w, int len, int fmt) {
+template <int FMT>
+__device__ __forceinline__ uint32_t block_codes(const uint32_t* __restrict__ words, int w, int len) {
     const int valid = len - 8 * w;
     if (valid <= 0) return 0xFFFFFFFFu;
-    uint32_t x = load_block8(words, w, fmt);
+    uint32_t x = load_block8(words, w, FMT);
     if (valid < 8) x |= 0xFFFFFFFFu << (4 * valid);
     return x;
 }
@@ -93,46 +94,56 @@ struct HalfInfo {
     int n, m, h0, p;  // p < 0: dummy half
 };
 
-// One chunk of the wavefront for both halves.  PASS 1: returns the lane's running maximum.
-// PASS 2: searches for the first cell equal to `target` (per half) and returns hit rows/cols.
+// Top/bottom rows of one chunk.  topX == nullptr: the table boundary (row -1) for half X.
+struct ChunkIO {
+    const uint32_t* topA_H;
+    const uint32_t* topA_F;
+    const uint32_t* topB_H;
+    const uint32_t* topB_F;
+    uint32_t* botH;  // nullptr: no spill (last chunk, or pass 2)
+    uint32_t* botF;
+};
+
+__device__ __forceinline__ void load8(const uint32_t* p, uint32_t (&v)[8]) {
+    const uint4 a = reinterpret_cast<const uint4*>(p)[0], b = reinterpret_cast<const uint4*>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// One chunk of the wavefront for both halves.  PASS 1 returns the lane's running maximum of the
+// diagonal candidates D (max H = max(0, max D): any positive H not reached through D is a gap value
+// strictly below an earlier cell).  PASS 2 searches the first cell equal to `target` per half.
 // rowA0 / rowB0: first target row of lane 0 of this chunk in each half (they differ in pass 2).
-template <int G, int MODE, bool PASS2>
+template <int G, int MODE, int FMT, bool PASS2>
 __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned mask, const int k, const int Q,
                                               const HalfInfo& A, const HalfInfo& B,
-                                              const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
                                               const uint32_t* __restrict__ twA, const uint32_t* __restrict__ twB,
-                                              const int rowA0, const int rowB0,
-                                              const uint32_t* rdHA, const uint32_t* rdFA,  // top rows (nullptr: boundary)
-                                              const uint32_t* rdHB, const uint32_t* rdFB,
-                                              uint32_t* wrH, uint32_t* wrF,  // bottom rows out (nullptr: none)
-                                              const uint32_t target, int (&hit)[4]) {
+                                              const uint32_t* __restrict__ selbuf, const int rowA0, const int rowB0,
+                                              const ChunkIO io, const uint32_t target, int (&hit)[4]) {
     const int al = a.alpha, be = a.beta;
-    const uint32_t nbeta = pack2(-be, -be), nalpha = pack2(-al, -al);
+    const uint32_t nbeta = pack2(-be, -be), nalpha = pack2(-al, -al), noGap = pack2(-al - be, -al - be);
     uint32_t lam = 2;
     while (int(lam) < a.match + 1) lam <<= 1;
     const int rA = rowA0 + 8 * k, rB = rowB0 + 8 * k;  // my first row in each half
-    // row tables
     uint32_t tabA[8], tabB[8];
     {
-        const uint32_t ta = (rA < A.m) ? block_codes(twA, rA >> 3, A.m, a.fmt) : 0xFFFFFFFFu;
-        const uint32_t tb = (rB < B.m) ? block_codes(twB, rB >> 3, B.m, a.fmt) : 0xFFFFFFFFu;
+        const uint32_t ta = (rA < A.m) ? block_codes<FMT>(twA, rA >> 3, A.m) : 0xFFFFFFFFu;
+        const uint32_t tb = (rB < B.m) ? block_codes<FMT>(twB, rB >> 3, B.m) : 0xFFFFFFFFu;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             tabA[r] = row_table((ta >> (4 * r)) & 15u, a.match, a.mismatch);
             tabB[r] = row_table((tb >> (4 * r)) & 15u, a.match, a.mismatch);
         }
     }
-    // left boundary H(i,-1), E(i,-1) = 0, corner H(r0-1,-1)
     // Hl[r] = H(r, c-1); En[r] = E(r, c) = max(E(r, c-1) - beta, H(r, c-1) - alpha), kept one column
-    // ahead so that H - alpha is consumed immediately (no register for it).
+    // ahead so that H - alpha is consumed immediately.  E(i,0) = max(H(i,-1) - alpha, E(i,-1) - beta);
+    // taking E(i,-1) as "no gap" changes only non-positive E values, which never reach
+    // H = max(0, ...) (clamp neutrality).  Same for F(-1, j) below.
     uint32_t Hl[8], En[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
         const int ha = MODE ? max(0, A.h0 - al - be * (rA + r)) : 0;
         const int hb = MODE ? max(0, B.h0 - al - be * (rB + r)) : 0;
         Hl[r] = pack2(ha, hb);
-        // E(i,0) = max(H(i,-1) - alpha, E(i,-1) - beta); taking E(i,-1) as "no gap" changes only
-        // non-positive E values, which never reach H = max(0, ...) (clamp neutrality)
         En[r] = vadd(Hl[r], nalpha);
     }
     uint32_t corner;
@@ -145,7 +156,6 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
     uint32_t botH[8], botF[8];
 #pragma unroll
     for (int x = 0; x < 8; ++x) botH[x] = botF[x] = 0;
-    const bool lane_rows = (rA < A.m) || (rB < B.m);
     const int steps = Q + G - 1;
     for (int s = 0; s < steps; ++s) {
         const int w = s - k;
@@ -157,77 +167,62 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
         }
         if (k == 0 && w < Q) {
             // top row of the chunk: spilled row of the previous chunk, or the table boundary
-            uint32_t bhA[8], bfA[8], bhB[8], bfB[8];
-            if (rdHA) {
-                const uint4* ph = reinterpret_cast<const uint4*>(rdHA + 8 * w);
-                const uint4* pf = reinterpret_cast<const uint4*>(rdFA + 8 * w);
-                uint4 h0v = ph[0], h1v = ph[1], f0v = pf[0], f1v = pf[1];
-                bhA[0] = h0v.x; bhA[1] = h0v.y; bhA[2] = h0v.z; bhA[3] = h0v.w;
-                bhA[4] = h1v.x; bhA[5] = h1v.y; bhA[6] = h1v.z; bhA[7] = h1v.w;
-                bfA[0] = f0v.x; bfA[1] = f0v.y; bfA[2] = f0v.z; bfA[3] = f0v.w;
-                bfA[4] = f1v.x; bfA[5] = f1v.y; bfA[6] = f1v.z; bfA[7] = f1v.w;
+            if (io.topA_H) {
+                load8(io.topA_H + 8 * w, topH);
+                load8(io.topA_F + 8 * w, topF);
             } else {
 #pragma unroll
                 for (int x = 0; x < 8; ++x) {
                     const int j = 8 * w + x;
-                    bhA[x] = pack2(MODE ? max(0, A.h0 - al - be * j) : 0, MODE ? max(0, B.h0 - al - be * j) : 0);
-                    bfA[x] = pack2(-al - be, -al - be);
+                    topH[x] = pack2(MODE ? max(0, A.h0 - al - be * j) : 0, MODE ? max(0, B.h0 - al - be * j) : 0);
+                    topF[x] = noGap;
                 }
             }
-            if (PASS2 && rdHB != rdHA) {
-                if (rdHB) {
-                    const uint4* ph = reinterpret_cast<const uint4*>(rdHB + 8 * w);
-                    const uint4* pf = reinterpret_cast<const uint4*>(rdFB + 8 * w);
-                    uint4 h0v = ph[0], h1v = ph[1], f0v = pf[0], f1v = pf[1];
-                    bhB[0] = h0v.x; bhB[1] = h0v.y; bhB[2] = h0v.z; bhB[3] = h0v.w;
-                    bhB[4] = h1v.x; bhB[5] = h1v.y; bhB[6] = h1v.z; bhB[7] = h1v.w;
-                    bfB[0] = f0v.x; bfB[1] = f0v.y; bfB[2] = f0v.z; bfB[3] = f0v.w;
-                    bfB[4] = f1v.x; bfB[5] = f1v.y; bfB[6] = f1v.z; bfB[7] = f1v.w;
+            if (PASS2 && io.topB_H != io.topA_H) {  // high halves from half B's own checkpoint
+                uint32_t bh[8], bf[8];
+                if (io.topB_H) {
+                    load8(io.topB_H + 8 * w, bh);
+                    load8(io.topB_F + 8 * w, bf);
                 } else {
 #pragma unroll
                     for (int x = 0; x < 8; ++x) {
                         const int j = 8 * w + x;
-                        bhB[x] = pack2(MODE ? max(0, A.h0 - al - be * j) : 0, MODE ? max(0, B.h0 - al - be * j) : 0);
-                        bfB[x] = pack2(-al - be, -al - be);
+                        bh[x] = pack2(0, MODE ? max(0, B.h0 - al - be * j) : 0);
+                        bf[x] = noGap;
                     }
                 }
 #pragma unroll
-                for (int x = 0; x < 8; ++x) {  // low half from A's source, high half from B's
-                    topH[x] = prmt(bhA[x], bhB[x], 0x7610);
-                    topF[x] = prmt(bfA[x], bfB[x], 0x7610);
-                }
-            } else {
-#pragma unroll
                 for (int x = 0; x < 8; ++x) {
-                    topH[x] = bhA[x];
-                    topF[x] = bfA[x];
+                    topH[x] = prmt(topH[x], bh[x], 0x7610);
+                    topF[x] = prmt(topF[x], bf[x], 0x7610);
                 }
             }
         }
-        if (w >= 0 && w < Q && lane_rows) {
+        if (unsigned(w) < unsigned(Q)) {
             uint32_t sel[8];
-            make_selectors(block_codes(qwA, w, A.n, a.fmt), block_codes(qwB, w, B.n, a.fmt), sel);
+            load8(selbuf + 8 * w, sel);
 #pragma unroll
             for (int x = 0; x < 8; ++x) {
                 uint32_t hup = topH[x], fup = topF[x];
                 uint32_t haup = vadd(hup, nalpha);
                 uint32_t hdiag = (x == 0) ? corner : topH[x - 1];
+                uint32_t dprev = 0;
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
                     const uint32_t f = vaddmax(fup, nbeta, haup);
                     const uint32_t e = En[r];
                     const uint32_t sc = prmt(tabA[r], tabB[r], sel[x]);
-                    uint32_t h;
+                    uint32_t d;
                     if (MODE) {
                         // dead-zero (EXTEND): D = hdiag + s if hdiag > 0, else <= 0:
                         // D = min(hdiag + s, lambda * hdiag), lambda = 2^k >= match + 1.  hdiag >= 0 and
                         // lambda * hdiag <= 32767 (routing bound), so one 32-bit IMAD scales both halves.
-                        const uint32_t kd = hdiag * lam;
-                        h = vmax3relu(vaddmin(hdiag, sc, kd), e, f);
+                        d = vaddmin(hdiag, sc, hdiag * lam);
                     } else {
-                        h = vmax3relu(vadd(hdiag, sc), e, f);  // D on the FMA pipe, one ALU max
+                        d = vadd(hdiag, sc);  // FMA pipe
                     }
-                    const uint32_t ha = vadd(h, nalpha);
+                    const uint32_t h = vmax3relu(d, e, f);
+                    const uint32_t ha = vadd(h, nalpha);  // FMA pipe
                     hdiag = Hl[r];
                     Hl[r] = h;
                     En[r] = vaddmax(e, nbeta, ha);
@@ -235,10 +230,13 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                     haup = ha;
                     fup = f;
                     if (!PASS2) {
-                        if (r == 1) M0 = vmax3(M0, Hl[0], Hl[1]);
-                        if (r == 3) M1 = vmax3(M1, Hl[2], Hl[3]);
-                        if (r == 5) M2 = vmax3(M2, Hl[4], Hl[5]);
-                        if (r == 7) M3 = vmax3(M3, Hl[6], Hl[7]);
+                        if (r & 1) {
+                            if (r == 1) M0 = vmax3(M0, dprev, d);
+                            if (r == 3) M1 = vmax3(M1, dprev, d);
+                            if (r == 5) M2 = vmax3(M2, dprev, d);
+                            if (r == 7) M3 = vmax3(M3, dprev, d);
+                        }
+                        dprev = d;
                     }
                 }
                 botH[x] = hup;
@@ -264,9 +262,9 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                 }
             }
             corner = topH[7];
-            if (wrH && k == G - 1) {
-                uint4* ph = reinterpret_cast<uint4*>(wrH + 8 * w);
-                uint4* pf = reinterpret_cast<uint4*>(wrF + 8 * w);
+            if (io.botH && k == G - 1) {
+                uint4* ph = reinterpret_cast<uint4*>(io.botH + 8 * w);
+                uint4* pf = reinterpret_cast<uint4*>(io.botF + 8 * w);
                 ph[0] = make_uint4(botH[0], botH[1], botH[2], botH[3]);
                 ph[1] = make_uint4(botH[4], botH[5], botH[6], botH[7]);
                 pf[0] = make_uint4(botF[0], botF[1], botF[2], botF[3]);
@@ -277,7 +275,7 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
     return vmax(vmax(M0, M1), vmax(M2, M3));
 }
 
-template <int G, int MODE>
+template <int G, int MODE, int FMT>
 __global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bin) {
     const int lane = threadIdx.x & 31;
     const int k = lane & (G - 1);
@@ -285,7 +283,9 @@ __global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bi
     const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << sub_base);
     const int64_t slot = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
     const int64_t S = a.spill_stride;
-    uint32_t* const spill = reinterpret_cast<uint32_t*>(a.spill) + slot * 8 * S;  // 4 buffers x (H, F)
+    // per slot: 4 spill buffers x (H, F) rows, then the query selectors (8 words per block)
+    uint32_t* const spill = reinterpret_cast<uint32_t*>(a.spill) + slot * 9 * S;
+    uint32_t* const selbuf = spill + 8 * S;
 
     const int start = a.bin_start[bin];
     const int cnt = a.bin_start[bin + 1] - start;
@@ -313,6 +313,16 @@ __global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bi
         const int chunksA = (((A.m + 7) >> 3) + G - 1) / G, chunksB = (((B.m + 7) >> 3) + G - 1) / G;
         const int chunks = max(chunksA, chunksB);
 
+        // query selectors, once per work item (shared by every chunk and by pass 2)
+        for (int w = k; w < Q; w += G) {
+            uint32_t sel[8];
+            make_selectors(block_codes<FMT>(qwA, w, A.n), block_codes<FMT>(qwB, w, B.n), sel);
+            uint4* p = reinterpret_cast<uint4*>(selbuf + 8 * w);
+            p[0] = make_uint4(sel[0], sel[1], sel[2], sel[3]);
+            p[1] = make_uint4(sel[4], sel[5], sel[6], sel[7]);
+        }
+        __syncwarp(mask);
+
         // pass 1 -------------------------------------------------------------------------------
         const int floorA = MODE ? A.h0 : 0, floorB = MODE ? B.h0 : 0;
         int bestA = floorA, bestB = floorB;   // running maxima (strict improvement records chunk)
@@ -321,13 +331,14 @@ __global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bi
         int rd = -1, wr = 0;
         for (int c = 0; c < chunks; ++c) {
             const bool last = (c + 1 == chunks);
-            const uint32_t* rdH = rd >= 0 ? spill + (2 * rd) * S : nullptr;
-            const uint32_t* rdF = rd >= 0 ? spill + (2 * rd + 1) * S : nullptr;
-            uint32_t* wrH = last ? nullptr : spill + (2 * wr) * S;
-            uint32_t* wrF = last ? nullptr : spill + (2 * wr + 1) * S;
+            ChunkIO io;
+            io.topA_H = io.topB_H = rd >= 0 ? spill + (2 * rd) * S : nullptr;
+            io.topA_F = io.topB_F = rd >= 0 ? spill + (2 * rd + 1) * S : nullptr;
+            io.botH = last ? nullptr : spill + (2 * wr) * S;
+            io.botF = last ? nullptr : spill + (2 * wr + 1) * S;
             int dummy[4];
-            uint32_t m = run_chunk<G, MODE, false>(a, mask, k, Q, A, B, qwA, qwB, twA, twB, c * 8 * G, c * 8 * G,
-                                                   rdH, rdF, rdH, rdF, wrH, wrF, 0u, dummy);
+            uint32_t m = run_chunk<G, MODE, FMT, false>(a, mask, k, Q, A, B, twA, twB, selbuf, c * 8 * G, c * 8 * G,
+                                                        io, 0u, dummy);
 #pragma unroll
             for (int off = 1; off < G; off <<= 1) m = vmax(m, __shfl_xor_sync(mask, m, off, G));
             if (lo16(m) > bestA) {
@@ -354,13 +365,16 @@ __global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bi
         if (ckA >= 0 || ckB >= 0) {
             const int cA = ckA >= 0 ? ckA : ckB, cB = ckB >= 0 ? ckB : ckA;
             const int bA = ckA >= 0 ? bufA : bufB, bB = ckB >= 0 ? bufB : bufA;
-            const uint32_t* hA = bA >= 0 ? spill + (2 * bA) * S : nullptr;
-            const uint32_t* fA = bA >= 0 ? spill + (2 * bA + 1) * S : nullptr;
-            const uint32_t* hB = bB >= 0 ? spill + (2 * bB) * S : nullptr;
-            const uint32_t* fB = bB >= 0 ? spill + (2 * bB + 1) * S : nullptr;
+            ChunkIO io;
+            io.topA_H = bA >= 0 ? spill + (2 * bA) * S : nullptr;
+            io.topA_F = bA >= 0 ? spill + (2 * bA + 1) * S : nullptr;
+            io.topB_H = bB >= 0 ? spill + (2 * bB) * S : nullptr;
+            io.topB_F = bB >= 0 ? spill + (2 * bB + 1) * S : nullptr;
+            io.botH = io.botF = nullptr;
+            if (bA == bB && cA != cB) io.topB_H = io.topB_F = nullptr;  // unreachable: distinct chunks own distinct buffers
             const uint32_t target = pack2(ckA >= 0 ? bestA : 0x7FFF, ckB >= 0 ? bestB : 0x7FFF);
-            run_chunk<G, MODE, true>(a, mask, k, Q, A, B, qwA, qwB, twA, twB, cA * 8 * G, cB * 8 * G, hA, fA,
-                                     hB, fB, nullptr, nullptr, target, hit);
+            run_chunk<G, MODE, FMT, true>(a, mask, k, Q, A, B, twA, twB, selbuf, cA * 8 * G, cB * 8 * G, io, target,
+                                          hit);
             // first hit in row-major order across the subwarp (rows grow with the lane index)
 #pragma unroll
             for (int off = 1; off < G; off <<= 1) {
@@ -391,37 +405,28 @@ __global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bi
     }
 }
 
-template <int MODE>
-static void launch_i16_mode(int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s) {
+template <int MODE, int FMT>
+static const void* kptr16(int gidx) {
     switch (gidx) {
-    case 0: dp_i16_kernel<1, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
-    case 1: dp_i16_kernel<2, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
-    case 2: dp_i16_kernel<4, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
-    case 3: dp_i16_kernel<8, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
-    case 4: dp_i16_kernel<16, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
-    default: dp_i16_kernel<32, MODE><<<grid, I16_THREADS, 0, s>>>(a, bin); break;
+    case 0: return (const void*)dp_i16_kernel<1, MODE, FMT>;
+    case 1: return (const void*)dp_i16_kernel<2, MODE, FMT>;
+    case 2: return (const void*)dp_i16_kernel<4, MODE, FMT>;
+    case 3: return (const void*)dp_i16_kernel<8, MODE, FMT>;
+    case 4: return (const void*)dp_i16_kernel<16, MODE, FMT>;
+    default: return (const void*)dp_i16_kernel<32, MODE, FMT>;
     }
+}
+const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt) {
+    if (mode == SALOBA_EXTEND) return fmt == SALOBA_PACK2 ? kptr16<1, 2>(gidx) : kptr16<1, 4>(gidx);
+    return fmt == SALOBA_PACK2 ? kptr16<0, 2>(gidx) : kptr16<0, 4>(gidx);
 }
 
 void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s) {
-    if (mode == SALOBA_EXTEND) launch_i16_mode<1>(gidx, grid, a, bin, s);
-    else launch_i16_mode<0>(gidx, grid, a, bin, s);
+    const void* fn = dp_i16_kernel_ptr(mode, gidx, a.fmt);
+    AlignArgs args = a;
+    void* params[] = {&args, &bin};
+    cudaLaunchKernel(fn, dim3(grid), dim3(I16_THREADS), params, 0, s);
     count_launches(1);
-}
-
-template <int MODE>
-static const void* kptr16_mode(int gidx) {
-    switch (gidx) {
-    case 0: return (const void*)dp_i16_kernel<1, MODE>;
-    case 1: return (const void*)dp_i16_kernel<2, MODE>;
-    case 2: return (const void*)dp_i16_kernel<4, MODE>;
-    case 3: return (const void*)dp_i16_kernel<8, MODE>;
-    case 4: return (const void*)dp_i16_kernel<16, MODE>;
-    default: return (const void*)dp_i16_kernel<32, MODE>;
-    }
-}
-const void* dp_i16_kernel_ptr(int mode, int gidx) {
-    return mode == SALOBA_EXTEND ? kptr16_mode<1>(gidx) : kptr16_mode<0>(gidx);
 }
 
 }  // namespace saloba
