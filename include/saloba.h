@@ -142,14 +142,32 @@ int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word_off, const
 
 /* ---- end-to-end from host buffers ----------------------------------------------------------- */
 
-/* Host-resident ASCII pairs in, host results out: uploads in pipelined slices (pinned host
- * memory recommended), packs, aligns and downloads on `stream`, then synchronises it.
+/* Host-resident ASCII pairs in, host results out (the call a read mapper makes).  The batch is cut
+ * into slices; slice i+1 is uploaded on an internal copy stream while slice i is packed and aligned
+ * on `stream`, and results are downloaded as slices finish.  Host buffers should be pinned
+ * (cudaHostAlloc / torch pin_memory) for the copies to overlap.
  *   q_ascii, t_ascii  [host] uint8   concatenated sequences;  q_off, t_off [host] int64[n_pairs+1]
- *   h0                [host] int32[n_pairs] or NULL in LOCAL
- *   score, q_end, t_end [host] int32[n_pairs]
- *   host_status       [host] int64: -1 or smallest bad pair index (invalid base / empty / length)
- * Device memory is allocated and freed inside the call (this entry point is the convenience
- * API; the device entry points above are the allocation-free hot path). */
+ *   h0                [host] int32[n_pairs] (EXTEND) or NULL (LOCAL)
+ *   score, q_end, t_end [host] int32[n_pairs]      results in input order
+ *   host_status       [host] int64: -1 or the smallest bad pair index (invalid base, empty or
+ *                     over-long sequence, bad h0); outputs of such pairs are unspecified
+ * The call synchronises `stream` before returning. */
+typedef struct saloba_host_ctx saloba_host_ctx;
+
+/* Device buffers, streams and events for batches of up to max_pairs pairs, max_q_bytes /
+ * max_t_bytes ASCII bytes and queries of up to max_qlen bases, on `device`.  NULL on failure. */
+saloba_host_ctx* saloba_host_ctx_create(int64_t max_pairs, int64_t max_q_bytes, int64_t max_t_bytes,
+                                        int32_t max_qlen, int device);
+void saloba_host_ctx_destroy(saloba_host_ctx* ctx);
+
+/* Align one host batch with a context (allocation-free; SALOBA_EWORKSPACE if it exceeds the
+ * context's capacity). */
+int saloba_align_host_ctx(saloba_host_ctx* ctx, const uint8_t* q_ascii, const int64_t* q_off,
+                          const uint8_t* t_ascii, const int64_t* t_off, const int32_t* h0, int64_t n_pairs,
+                          saloba_scoring sc, saloba_mode mode, int32_t* score, int32_t* q_end, int32_t* t_end,
+                          int64_t* host_status, const saloba_options* opt, void* stream);
+
+/* Convenience: create a context sized for this batch, align, destroy. */
 int saloba_align_host(const uint8_t* q_ascii, const int64_t* q_off, const uint8_t* t_ascii, const int64_t* t_off,
                       const int32_t* h0, int64_t n_pairs, saloba_scoring sc, saloba_mode mode, int32_t* score,
                       int32_t* q_end, int32_t* t_end, int64_t* host_status, const saloba_options* opt,

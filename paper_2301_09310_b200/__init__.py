@@ -24,7 +24,8 @@ OK, EINVAL, ECUDA, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4
 
 #: every symbol include/saloba.h declares
 EXPORTS = ("saloba_packed_words", "saloba_pack", "saloba_workspace_bytes", "saloba_align_batch",
-           "saloba_align_host", "saloba_strerror", "saloba_version", "saloba_kernel_launches")
+           "saloba_host_ctx_create", "saloba_host_ctx_destroy", "saloba_align_host_ctx", "saloba_align_host",
+           "saloba_strerror", "saloba_version", "saloba_kernel_launches")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libsaloba.so")
@@ -105,6 +106,12 @@ def lib() -> ctypes.CDLL:
         L.saloba_align_host.argtypes = [vp, vp, vp, vp, vp, i64, _Scoring, ctypes.c_int, vp, vp, vp, vp,
                                         ctypes.POINTER(_Options), vp]
         L.saloba_align_host.restype = ctypes.c_int
+        L.saloba_host_ctx_create.argtypes = [i64, i64, i64, i32, ctypes.c_int]
+        L.saloba_host_ctx_create.restype = vp
+        L.saloba_host_ctx_destroy.argtypes = [vp]
+        L.saloba_host_ctx_destroy.restype = None
+        L.saloba_align_host_ctx.argtypes = [vp] + list(L.saloba_align_host.argtypes)
+        L.saloba_align_host_ctx.restype = ctypes.c_int
         L.saloba_strerror.argtypes = [ctypes.c_int]
         L.saloba_strerror.restype = ctypes.c_char_p
         L.saloba_version.restype = ctypes.c_int
@@ -221,7 +228,7 @@ def align(q_ascii, q_off, t_ascii, t_off, h0=None, scoring: Scoring = BWA_MEM, m
 
 
 def align_host(batch, scoring: Scoring = BWA_MEM, mode: int = LOCAL, options: Options | None = None,
-               out=None, stream=None):
+               out=None, stream=None, ctx: "HostContext | None" = None):
     """End-to-end from host buffers (numpy / pinned CPU tensors): returns numpy-like int32 arrays
     (score, q_end, t_end) and the host status (-1 or first bad pair)."""
     import numpy as np
@@ -241,10 +248,14 @@ def align_host(batch, scoring: Scoring = BWA_MEM, mode: int = LOCAL, options: Op
     to = np.ascontiguousarray(batch.t_off, np.int64)
     h0 = np.ascontiguousarray(batch.h0, np.int32) if mode == EXTEND else None
     o = out if isinstance(out, np.ndarray) else out.numpy()
-    rc = lib().saloba_align_host(host_ptr(batch.q_ascii), host_ptr(qo), host_ptr(batch.t_ascii), host_ptr(to),
-                                 host_ptr(h0) if h0 is not None else None, n, scoring._c(), mode,
-                                 ctypes.c_void_p(o[0].ctypes.data), ctypes.c_void_p(o[1].ctypes.data),
-                                 ctypes.c_void_p(o[2].ctypes.data), ctypes.byref(st), opt, _stream(stream))
+    args = (host_ptr(batch.q_ascii), host_ptr(qo), host_ptr(batch.t_ascii), host_ptr(to),
+            host_ptr(h0) if h0 is not None else None, n, scoring._c(), mode,
+            ctypes.c_void_p(o[0].ctypes.data), ctypes.c_void_p(o[1].ctypes.data),
+            ctypes.c_void_p(o[2].ctypes.data), ctypes.byref(st), opt, _stream(stream))
+    if ctx is not None:
+        rc = lib().saloba_align_host_ctx(ctypes.c_void_p(ctx.handle), *args)
+    else:
+        rc = lib().saloba_align_host(*args)
     _check(rc, "saloba_align_host")
     return o[0, :n], o[1, :n], o[2, :n], int(st.value)
 
@@ -290,3 +301,24 @@ class Aligner:
                                   ctypes.c_void_p(self.status.data_ptr() + 16), opt, st)
         _check(rc, "saloba_align_batch")
         return self.out[0, :n], self.out[1, :n], self.out[2, :n]
+
+
+class HostContext:
+    """Reusable device buffers/streams for the host-buffer entry point (saloba_host_ctx)."""
+
+    def __init__(self, max_pairs: int, max_q_bytes: int, max_t_bytes: int, max_qlen: int, device=None):
+        dev = torch.cuda.current_device() if device is None else device
+        self.handle = lib().saloba_host_ctx_create(max_pairs, max_q_bytes, max_t_bytes, max_qlen, dev)
+        if not self.handle:
+            raise SalobaError(ECUDA, "saloba_host_ctx_create")
+
+    def close(self):
+        if self.handle:
+            lib().saloba_host_ctx_destroy(ctypes.c_void_p(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -235,17 +235,88 @@ SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word
 }
 
 // ---- end-to-end from host buffers -----------------------------------------------------------
-namespace {
-struct DevBuf {
-    void* p = nullptr;
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
-    cudaError_t alloc(size_t n) { return cudaMalloc(&p, std::max<size_t>(n, 256)); }
+namespace saloba {
+__global__ void rebase_offsets(int64_t* off, int64_t n, int64_t base) {
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
+        off[k] -= base;
+}
+}  // namespace saloba
+
+constexpr int HOST_SLICES = 8;
+
+struct saloba_host_ctx {
+    int device = 0;
+    int64_t max_pairs = 0, max_q_bytes = 0, max_t_bytes = 0;
+    int32_t max_qlen = 0;
+    int64_t slice_pairs = 0;
+    size_t ws_bytes = 0;
+    void *q = nullptr, *t = nullptr, *qo = nullptr, *to = nullptr, *qw = nullptr, *tw = nullptr, *qwo = nullptr,
+         *two = nullptr, *ql = nullptr, *tl = nullptr, *h0 = nullptr, *res = nullptr, *ws = nullptr, *st = nullptr;
+    int64_t qwcap = 0, twcap = 0;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t up[HOST_SLICES], done[HOST_SLICES];
+    int64_t* hst = nullptr;  // pinned status readback
 };
 
-int64_t first_pair_of_byte(const int64_t* off, int64_t n, int64_t byte) {
-    // pair k with off[k] <= byte < off[k+1]
+SALOBA_API void saloba_host_ctx_destroy(saloba_host_ctx* c) {
+    if (!c) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    void* bufs[] = {c->q, c->t, c->qo, c->to, c->qw, c->tw, c->qwo, c->two, c->ql, c->tl, c->h0, c->res, c->ws, c->st};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    if (c->copy) {
+        for (int i = 0; i < HOST_SLICES; ++i) {
+            cudaEventDestroy(c->up[i]);
+            cudaEventDestroy(c->done[i]);
+        }
+        cudaStreamDestroy(c->copy);
+    }
+    if (c->hst) cudaFreeHost(c->hst);
+    cudaSetDevice(prev);
+    delete c;
+}
+
+SALOBA_API saloba_host_ctx* saloba_host_ctx_create(int64_t max_pairs, int64_t max_q_bytes, int64_t max_t_bytes,
+                                                   int32_t max_qlen, int device) {
+    if (max_pairs < 0 || max_q_bytes < 0 || max_t_bytes < 0 || max_qlen < 1) return nullptr;
+    int prev = 0;
+    if (cudaGetDevice(&prev) != cudaSuccess || cudaSetDevice(device) != cudaSuccess) return nullptr;
+    saloba_host_ctx* c = new saloba_host_ctx();
+    c->device = device;
+    c->max_pairs = max_pairs;
+    c->max_q_bytes = max_q_bytes;
+    c->max_t_bytes = max_t_bytes;
+    c->max_qlen = max_qlen;
+    c->slice_pairs = (max_pairs + HOST_SLICES - 1) / HOST_SLICES;
+    c->qwcap = saloba_packed_words(max_q_bytes, max_pairs, SALOBA_PACK4);
+    c->twcap = saloba_packed_words(max_t_bytes, max_pairs, SALOBA_PACK4);
+    c->ws_bytes = saloba_workspace_bytes(std::max<int64_t>(c->slice_pairs, 1), max_qlen, 0, device);
+    auto al = [](void** p, size_t n) { return cudaMalloc(p, std::max<size_t>(n, 256)) == cudaSuccess; };
+    const int64_t np1 = max_pairs + 1;
+    bool ok = c->ws_bytes > 0 && al(&c->q, max_q_bytes) && al(&c->t, max_t_bytes) && al(&c->qo, np1 * 8) &&
+              al(&c->to, np1 * 8) && al(&c->qw, c->qwcap * 4) && al(&c->tw, c->twcap * 4) && al(&c->qwo, np1 * 8) &&
+              al(&c->two, np1 * 8) && al(&c->ql, max_pairs * 4) && al(&c->tl, max_pairs * 4) &&
+              al(&c->h0, max_pairs * 4) && al(&c->res, max_pairs * 12) && al(&c->ws, c->ws_bytes) &&
+              al(&c->st, 4 * HOST_SLICES * 8) &&
+              cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaMallocHost((void**)&c->hst, 4 * HOST_SLICES * 8) == cudaSuccess;
+    if (ok && c->copy)
+        for (int i = 0; i < HOST_SLICES; ++i) {
+            cudaEventCreateWithFlags(&c->up[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&c->done[i], cudaEventDisableTiming);
+        }
+    cudaSetDevice(prev);
+    if (!ok) {
+        saloba_host_ctx_destroy(c);
+        return nullptr;
+    }
+    return c;
+}
+
+namespace {
+int64_t pair_of_byte(const int64_t* off, int64_t n, int64_t byte) {  // k with off[k] <= byte < off[k+1]
     int64_t lo = 0, hi = n - 1;
     while (lo < hi) {
         int64_t mid = (lo + hi + 1) / 2;
@@ -256,110 +327,102 @@ int64_t first_pair_of_byte(const int64_t* off, int64_t n, int64_t byte) {
 }
 }  // namespace
 
-SALOBA_API int saloba_align_host(const uint8_t* q_ascii, const int64_t* q_off, const uint8_t* t_ascii,
-                                 const int64_t* t_off, const int32_t* h0, int64_t n_pairs, saloba_scoring sc,
-                                 saloba_mode mode, int32_t* score, int32_t* q_end, int32_t* t_end,
-                                 int64_t* host_status, const saloba_options* opt, void* stream) {
-    if (n_pairs < 0 || !q_off || !t_off || !host_status) return SALOBA_EINVAL;
+SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii, const int64_t* q_off,
+                                     const uint8_t* t_ascii, const int64_t* t_off, const int32_t* h0, int64_t n_pairs,
+                                     saloba_scoring sc, saloba_mode mode, int32_t* score, int32_t* q_end,
+                                     int32_t* t_end, int64_t* host_status, const saloba_options* opt, void* stream) {
+    if (!c || n_pairs < 0 || !q_off || !t_off || !host_status) return SALOBA_EINVAL;
     if (n_pairs > 0 && (!q_ascii || !t_ascii || !score || !q_end || !t_end)) return SALOBA_EINVAL;
     if (mode == SALOBA_EXTEND && n_pairs > 0 && !h0) return SALOBA_EINVAL;
     if (!scheme_ok(sc)) return SALOBA_EINVAL;
     *host_status = -1;
     if (n_pairs == 0) return SALOBA_OK;
+    const int64_t qb0 = q_off[0], tb0 = t_off[0];
+    const int64_t qbytes = q_off[n_pairs] - qb0, tbytes = t_off[n_pairs] - tb0;
+    if (n_pairs > c->max_pairs || qbytes > c->max_q_bytes || tbytes > c->max_t_bytes) return SALOBA_EWORKSPACE;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
     cudaStream_t s = (cudaStream_t)stream;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return SALOBA_ECUDA;
 
-    const int64_t qbytes = q_off[n_pairs] - q_off[0], tbytes = t_off[n_pairs] - t_off[0];
-    int32_t max_q = 1;
-    for (int64_t k = 0; k < n_pairs; ++k) max_q = std::max<int32_t>(max_q, int32_t(q_off[k + 1] - q_off[k]));
+    const int nsl = int(std::min<int64_t>(HOST_SLICES, n_pairs));
+    int64_t cut[HOST_SLICES + 1];
+    for (int i = 0; i <= nsl; ++i) cut[i] = n_pairs * i / nsl;
+    uint8_t* qd = static_cast<uint8_t*>(c->q);
+    uint8_t* td = static_cast<uint8_t*>(c->t);
+    int64_t* qo = static_cast<int64_t*>(c->qo);
+    int64_t* to = static_cast<int64_t*>(c->to);
+    int64_t* st = static_cast<int64_t*>(c->st);
+    int32_t* res = static_cast<int32_t*>(c->res);
+    int32_t* h0d = h0 ? static_cast<int32_t*>(c->h0) : nullptr;
 
-    // slices of ~equal bytes, at least 4 MB each, up to 8
-    const int64_t total = qbytes + tbytes;
-    int nslices = int(std::min<int64_t>(8, std::max<int64_t>(1, total / (4 << 20))));
-    nslices = int(std::min<int64_t>(nslices, n_pairs));
-    std::vector<int64_t> cut(nslices + 1);
-    for (int i = 0; i <= nslices; ++i) cut[i] = n_pairs * i / nslices;
-    int64_t max_slice = 0;
-    for (int i = 0; i < nslices; ++i) max_slice = std::max(max_slice, cut[i + 1] - cut[i]);
-
-    DevBuf dq, dt, dqo, dto, dqw, dtw, dqwo, dtwo, dql, dtl, dh0, dres, dws, dst;
-    const int64_t qwcap = saloba_packed_words(qbytes, n_pairs, SALOBA_PACK4);
-    const int64_t twcap = saloba_packed_words(tbytes, n_pairs, SALOBA_PACK4);
-    const size_t wsb = saloba_workspace_bytes(max_slice, max_q, 0, dev);
-    if (dq.alloc(qbytes) || dt.alloc(tbytes) || dqo.alloc((n_pairs + 1) * 8) || dto.alloc((n_pairs + 1) * 8) ||
-        dqw.alloc(qwcap * 4) || dtw.alloc(twcap * 4) || dqwo.alloc((n_pairs + 1) * 8) ||
-        dtwo.alloc((n_pairs + 1) * 8) || dql.alloc(n_pairs * 4) || dtl.alloc(n_pairs * 4) ||
-        dh0.alloc(n_pairs * 4) || dres.alloc(n_pairs * 12) || dws.alloc(wsb) || dst.alloc(64 * 8))
-        return SALOBA_ECUDA;
-
-    // device offsets relative to the start of each host buffer
-    std::vector<int64_t> qo(n_pairs + 1), to(n_pairs + 1);
-    for (int64_t k = 0; k <= n_pairs; ++k) {
-        qo[k] = q_off[k] - q_off[0];
-        to[k] = t_off[k] - t_off[0];
+    // offsets (8 B per pair) and h0 first; rebased on the device so the host never touches them
+    cudaMemcpyAsync(qo, q_off, (n_pairs + 1) * 8, cudaMemcpyHostToDevice, c->copy);
+    cudaMemcpyAsync(to, t_off, (n_pairs + 1) * 8, cudaMemcpyHostToDevice, c->copy);
+    if (h0) cudaMemcpyAsync(h0d, h0, n_pairs * 4, cudaMemcpyHostToDevice, c->copy);
+    if (qb0 || tb0) {
+        rebase_offsets<<<64, 256, 0, c->copy>>>(qo, n_pairs + 1, qb0);
+        rebase_offsets<<<64, 256, 0, c->copy>>>(to, n_pairs + 1, tb0);
+        count_launches(2);
     }
-    uint8_t* q_base = static_cast<uint8_t*>(dq.p);
-    uint8_t* t_base = static_cast<uint8_t*>(dt.p);
-    int64_t* st = static_cast<int64_t*>(dst.p);
-    int32_t* res = static_cast<int32_t*>(dres.p);
-
-    cudaStream_t cs = nullptr;
-    cudaEvent_t ev_up[8], ev_done[8];
-    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return SALOBA_ECUDA;
-    for (int i = 0; i < nslices; ++i) {
-        cudaEventCreateWithFlags(&ev_up[i], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming);
-    }
-    // offsets (small) first, synchronously ordered on the copy stream
-    cudaMemcpyAsync(dqo.p, qo.data(), (n_pairs + 1) * 8, cudaMemcpyHostToDevice, cs);
-    cudaMemcpyAsync(dto.p, to.data(), (n_pairs + 1) * 8, cudaMemcpyHostToDevice, cs);
-    if (h0) cudaMemcpyAsync(dh0.p, h0, n_pairs * 4, cudaMemcpyHostToDevice, cs);
-    const int32_t* dh0p = h0 ? static_cast<int32_t*>(dh0.p) : nullptr;
     int rc = SALOBA_OK;
-    for (int i = 0; i < nslices && rc == SALOBA_OK; ++i) {
+    for (int i = 0; i < nsl && rc == SALOBA_OK; ++i) {
         const int64_t a0 = cut[i], a1 = cut[i + 1], na = a1 - a0;
-        cudaMemcpyAsync(q_base + qo[a0], q_ascii + q_off[a0], qo[a1] - qo[a0], cudaMemcpyHostToDevice, cs);
-        cudaMemcpyAsync(t_base + to[a0], t_ascii + t_off[a0], to[a1] - to[a0], cudaMemcpyHostToDevice, cs);
-        cudaEventRecord(ev_up[i], cs);
-        cudaStreamWaitEvent(s, ev_up[i], 0);
-        launch_pack_range(q_base, static_cast<int64_t*>(dqo.p) + a0, na, a0, SALOBA_PACK4,
-                          static_cast<uint32_t*>(dqw.p), static_cast<int64_t*>(dqwo.p) + a0,
-                          static_cast<int32_t*>(dql.p) + a0, st + 4 * i + 0, s);
-        launch_pack_range(t_base, static_cast<int64_t*>(dto.p) + a0, na, a0, SALOBA_PACK4,
-                          static_cast<uint32_t*>(dtw.p), static_cast<int64_t*>(dtwo.p) + a0,
-                          static_cast<int32_t*>(dtl.p) + a0, st + 4 * i + 1, s);
-        rc = saloba_align_batch(static_cast<uint32_t*>(dqw.p), static_cast<int64_t*>(dqwo.p) + a0,
-                                static_cast<int32_t*>(dql.p) + a0, static_cast<uint32_t*>(dtw.p),
-                                static_cast<int64_t*>(dtwo.p) + a0, static_cast<int32_t*>(dtl.p) + a0,
-                                dh0p ? dh0p + a0 : nullptr, na, sc, mode, SALOBA_PACK4, res + a0,
-                                res + n_pairs + a0, res + 2 * n_pairs + a0, dws.p, wsb, st + 4 * i + 2, opt, s);
-        cudaEventRecord(ev_done[i], s);
-        cudaStreamWaitEvent(cs, ev_done[i], 0);
-        cudaMemcpyAsync(score + a0, res + a0, na * 4, cudaMemcpyDeviceToHost, cs);
-        cudaMemcpyAsync(q_end + a0, res + n_pairs + a0, na * 4, cudaMemcpyDeviceToHost, cs);
-        cudaMemcpyAsync(t_end + a0, res + 2 * n_pairs + a0, na * 4, cudaMemcpyDeviceToHost, cs);
+        const int64_t qs = q_off[a0] - qb0, qe = q_off[a1] - qb0, ts = t_off[a0] - tb0, te = t_off[a1] - tb0;
+        cudaMemcpyAsync(qd + qs, q_ascii + q_off[a0], qe - qs, cudaMemcpyHostToDevice, c->copy);
+        cudaMemcpyAsync(td + ts, t_ascii + t_off[a0], te - ts, cudaMemcpyHostToDevice, c->copy);
+        cudaEventRecord(c->up[i], c->copy);
+        cudaStreamWaitEvent(s, c->up[i], 0);
+        launch_pack_range(qd, qo + a0, na, a0, SALOBA_PACK4, static_cast<uint32_t*>(c->qw),
+                          static_cast<int64_t*>(c->qwo) + a0, static_cast<int32_t*>(c->ql) + a0, st + 4 * i + 0, s);
+        launch_pack_range(td, to + a0, na, a0, SALOBA_PACK4, static_cast<uint32_t*>(c->tw),
+                          static_cast<int64_t*>(c->two) + a0, static_cast<int32_t*>(c->tl) + a0, st + 4 * i + 1, s);
+        rc = saloba_align_batch(static_cast<uint32_t*>(c->qw), static_cast<int64_t*>(c->qwo) + a0,
+                                static_cast<int32_t*>(c->ql) + a0, static_cast<uint32_t*>(c->tw),
+                                static_cast<int64_t*>(c->two) + a0, static_cast<int32_t*>(c->tl) + a0,
+                                h0d ? h0d + a0 : nullptr, na, sc, mode, SALOBA_PACK4, res + a0, res + n_pairs + a0,
+                                res + 2 * n_pairs + a0, c->ws, c->ws_bytes, st + 4 * i + 2, opt, s);
+        cudaEventRecord(c->done[i], s);
+        cudaStreamWaitEvent(c->copy, c->done[i], 0);
+        cudaMemcpyAsync(score + a0, res + a0, na * 4, cudaMemcpyDeviceToHost, c->copy);
+        cudaMemcpyAsync(q_end + a0, res + n_pairs + a0, na * 4, cudaMemcpyDeviceToHost, c->copy);
+        cudaMemcpyAsync(t_end + a0, res + 2 * n_pairs + a0, na * 4, cudaMemcpyDeviceToHost, c->copy);
     }
-    int64_t hst[64];
-    cudaMemcpyAsync(hst, st, sizeof(int64_t) * 4 * nslices, cudaMemcpyDeviceToHost, cs);
-    cudaError_t e = cudaStreamSynchronize(cs);
+    cudaMemcpyAsync(c->hst, st, sizeof(int64_t) * 4 * nsl, cudaMemcpyDeviceToHost, c->copy);
+    const cudaError_t e = cudaStreamSynchronize(c->copy);
     cudaStreamSynchronize(s);
-    for (int i = 0; i < nslices; ++i) {
-        cudaEventDestroy(ev_up[i]);
-        cudaEventDestroy(ev_done[i]);
-    }
-    cudaStreamDestroy(cs);
+    cudaSetDevice(prev);
     if (rc != SALOBA_OK) return rc;
     if (e != cudaSuccess) return SALOBA_ECUDA;
-    // status: smallest bad pair over all slices (invalid byte -> its pair; align status is slice-local)
     int64_t bad = INT64_MAX;
-    for (int i = 0; i < nslices; ++i) {
-        if (hst[4 * i + 0] >= 0) bad = std::min(bad, first_pair_of_byte(qo.data(), n_pairs, hst[4 * i + 0]));
-        if (hst[4 * i + 1] >= 0) bad = std::min(bad, first_pair_of_byte(to.data(), n_pairs, hst[4 * i + 1]));
-        if (hst[4 * i + 2] >= 0) bad = std::min(bad, cut[i] + hst[4 * i + 2]);
+    for (int i = 0; i < nsl; ++i) {
+        if (c->hst[4 * i + 0] >= 0) bad = std::min(bad, pair_of_byte(q_off, n_pairs, c->hst[4 * i + 0] + qb0));
+        if (c->hst[4 * i + 1] >= 0) bad = std::min(bad, pair_of_byte(t_off, n_pairs, c->hst[4 * i + 1] + tb0));
+        if (c->hst[4 * i + 2] >= 0) bad = std::min(bad, cut[i] + c->hst[4 * i + 2]);
     }
     *host_status = bad == INT64_MAX ? -1 : bad;
     return SALOBA_OK;
+}
+
+SALOBA_API int saloba_align_host(const uint8_t* q_ascii, const int64_t* q_off, const uint8_t* t_ascii,
+                                 const int64_t* t_off, const int32_t* h0, int64_t n_pairs, saloba_scoring sc,
+                                 saloba_mode mode, int32_t* score, int32_t* q_end, int32_t* t_end,
+                                 int64_t* host_status, const saloba_options* opt, void* stream) {
+    if (n_pairs < 0 || !q_off || !t_off || !host_status) return SALOBA_EINVAL;
+    if (n_pairs == 0) {
+        *host_status = -1;
+        return SALOBA_OK;
+    }
+    int32_t max_q = 1;
+    for (int64_t k = 0; k < n_pairs; ++k) max_q = std::max<int32_t>(max_q, int32_t(q_off[k + 1] - q_off[k]));
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return SALOBA_ECUDA;
+    saloba_host_ctx* c = saloba_host_ctx_create(n_pairs, q_off[n_pairs] - q_off[0], t_off[n_pairs] - t_off[0], max_q, dev);
+    if (!c) return SALOBA_ECUDA;
+    const int rc = saloba_align_host_ctx(c, q_ascii, q_off, t_ascii, t_off, h0, n_pairs, sc, mode, score, q_end, t_end,
+                                         host_status, opt, stream);
+    saloba_host_ctx_destroy(c);
+    return rc;
 }
 
 SALOBA_API const char* saloba_strerror(int code) {

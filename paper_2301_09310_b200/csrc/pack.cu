@@ -3,86 +3,126 @@
 //
 // Layout (closed form, no scan): sequence s occupies words [byte_off[s]/B + s, ...) with
 // B = 8 (PACK4) or 16 (PACK2); ceil(len/B) <= floor(end/B) - floor(start/B) + 1 words fit.
-// One warp per sequence, one lane per output word: the warp reads 256 contiguous bytes per
-// instruction (32 lanes x 8 bytes), so reads coalesce; 4-bit output words coalesce likewise.
+// A warp packs tiles of 8 consecutive sequences with lanes over the tile's flattened words, so
+// reads (8 bytes per lane) and 4-bit word writes coalesce and short sequences leave no lane idle.
 #include "common.cuh"
 
 namespace saloba {
 
-// code table: A/a 0, C/c 1, G/g 2, T/t/U/u 3, N/n 4, anything else 0xFF (invalid)
-__device__ __forceinline__ uint32_t base_code(uint32_t b) {
-    uint32_t u = b & 0xDF;  // upper-case ASCII letters
-    uint32_t c = 0xFF;
-    c = (u == 'A') ? 0u : c;
-    c = (u == 'C') ? 1u : c;
-    c = (u == 'G') ? 2u : c;
-    c = (u == 'T' || u == 'U') ? 3u : c;
-    c = (u == 'N') ? 4u : c;
-    // reject non-letters that alias after the case fold (e.g. 'A' ^ 0x20 = 'a' is fine, but 0x01 etc.)
-    c = ((b | 0x20) >= 'a' && (b | 0x20) <= 'z') ? c : 0xFFu;
-    return c;
-}
-
-__device__ __forceinline__ uint64_t load8_unaligned(const uint8_t* __restrict__ base, int64_t pos, int64_t total) {
-    // 8 bytes starting at base[pos] (bytes beyond `total` are returned as 0)
-    int64_t a = pos & ~int64_t(7);
-    int sh = int(pos & 7) * 8;
-    if (a + 16 <= total) {
-        uint64_t lo = __ldg(reinterpret_cast<const unsigned long long*>(base + a));
-        uint64_t hi = __ldg(reinterpret_cast<const unsigned long long*>(base + a + 8));
-        return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+// Byte -> code table (A/a 0, C/c 1, G/g 2, T/t/U/u 3, N/n 4 [PACK4 only], else 0xFF = invalid),
+// staged in shared memory per block; lookups of ASCII letters hit distinct banks.
+__device__ __forceinline__ void build_lut(uint8_t* lut, int bits) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        const int u = i & 0xDF;
+        const bool letter = ((i | 0x20) >= 'a' && (i | 0x20) <= 'z');
+        uint8_t c = 0xFF;
+        if (letter) {
+            if (u == 'A') c = 0;
+            else if (u == 'C') c = 1;
+            else if (u == 'G') c = 2;
+            else if (u == 'T' || u == 'U') c = 3;
+            else if (u == 'N' && bits == 4) c = 4;
+        }
+        lut[i] = c;
     }
-    uint64_t r = 0;
-    for (int k = 0; k < 8; ++k)
-        if (pos + k < total) r |= uint64_t(base[pos + k]) << (8 * k);
-    return r;
 }
 
+// 8 bytes starting at base[pos] (only bytes < total are read; others come back as 0)
+__device__ __forceinline__ uint2 load8(const uint8_t* __restrict__ base, int64_t pos, int64_t total) {
+    const int64_t a = pos & ~int64_t(3);
+    const int sh = int(pos & 3) * 8;
+    if (a + 12 <= total) {
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(base + a);
+        const uint32_t w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2);
+        return make_uint2(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh));
+    }
+    uint32_t lo = 0, hi = 0;
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t b = (pos + k < total) ? base[pos + k] : 0u;
+        if (k < 4) lo |= b << (8 * k);
+        else hi |= b << (8 * (k - 4));
+    }
+    return make_uint2(lo, hi);
+}
+
+// One warp packs a tile of up to 8 consecutive sequences: lanes sweep the tile's words (flattened
+// across sequence boundaries) so short sequences do not leave lanes idle.  Per base: one byte
+// extract (ALU), one shared-memory table lookup (MIO) and one shift-accumulate.
 template <int BITS>
 __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ ascii, const int64_t* __restrict__ byte_off,
                                                    int64_t n_seqs, int64_t base, uint32_t* __restrict__ words,
                                                    int64_t* __restrict__ word_off, int32_t* __restrict__ lens,
                                                    unsigned long long* __restrict__ status) {
     constexpr int B = 32 / BITS;  // bases per word
+    constexpr int SPT = 8;        // sequences per warp tile
+    __shared__ uint8_t lut[256];
+    build_lut(lut, BITS);
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     const int64_t total = byte_off[n_seqs];  // ascii is readable up to here
-    for (int64_t s = warp; s < n_seqs; s += nwarps) {
-        const int64_t b0 = byte_off[s], b1 = byte_off[s + 1];
-        const int64_t len = b1 - b0;
-        const int64_t w0 = b0 / B + s + base;
-        if (lane == 0) {
+    for (int64_t s0 = warp * SPT; s0 < n_seqs; s0 += nwarps * SPT) {
+        // lanes 0..SPT-1 describe one sequence each
+        int64_t b0 = 0, len = 0, w0 = 0;
+        int nw = 0;
+        const int64_t s = s0 + lane;
+        if (lane < SPT && s < n_seqs) {
+            b0 = byte_off[s];
+            len = byte_off[s + 1] - b0;
+            w0 = b0 / B + s + base;
+            nw = int((len + B - 1) / B);
             word_off[s] = w0;
             if (lens) lens[s] = int32_t(len);
             if (s == n_seqs - 1) word_off[n_seqs] = byte_off[n_seqs] / B + n_seqs + base;
         }
-        const int64_t nw = (len + B - 1) / B;
-        for (int64_t w = lane; w < nw; w += 32) {
-            uint32_t out = 0;
-            unsigned long long bad = ~0ull;
+        // inclusive scan of word counts over the tile
+        int incl = nw;
+#pragma unroll
+        for (int off = 1; off < SPT; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const int tile_words = __shfl_sync(0xffffffffu, incl, SPT - 1);
+        for (int fb = 0; fb < tile_words; fb += 32) {  // all lanes iterate: shuffles stay converged
+            const int f = fb + lane;
+            // sequence i of the tile holding flattened word f
+            int i = 0;
+#pragma unroll
+            for (int j = 0; j < SPT - 1; ++j) i += (f >= __shfl_sync(0xffffffffu, incl, j)) ? 1 : 0;
+            if (i > SPT - 1) i = SPT - 1;
+            const int start = __shfl_sync(0xffffffffu, incl - nw, i);
+            const int64_t sb0 = __shfl_sync(0xffffffffu, b0, i);
+            const int64_t slen = __shfl_sync(0xffffffffu, len, i);
+            const int64_t sw0 = __shfl_sync(0xffffffffu, w0, i);
+            if (f >= tile_words) continue;
+            const int w = f - start;
+            uint32_t out = 0, bad = 0;
 #pragma unroll
             for (int half = 0; half < B / 8; ++half) {
-                const int64_t p0 = w * B + half * 8;  // first base of this 8-base group
-                uint64_t bytes = load8_unaligned(ascii, b0 + p0, total);
+                const int64_t p0 = int64_t(w) * B + half * 8;
+                const uint2 by = load8(ascii, sb0 + p0, total);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
-                    const int64_t p = p0 + c;
-                    uint32_t code;
-                    if (p < len) {
-                        code = base_code(uint32_t(bytes >> (8 * c)) & 0xFF);
-                        if (code == 0xFF || (BITS == 2 && code == 4)) {
-                            if (bad == ~0ull) bad = (unsigned long long)(b0 + p);
-                            code = BITS == 4 ? 15u : 0u;
-                        }
-                    } else {
-                        code = BITS == 4 ? 15u : 0u;  // padding (never scored)
-                    }
+                    const uint32_t byte = ((c < 4 ? by.x : by.y) >> (8 * (c & 3))) & 0xFFu;
+                    uint32_t code = lut[byte];
+                    const bool valid = p0 + c < slen;
+                    if (valid) bad |= code;
+                    if (!valid || code == 0xFFu) code = BITS == 4 ? 15u : 0u;  // padding / invalid
                     out |= code << (BITS * (half * 8 + c));
                 }
             }
-            words[w0 + w] = out;
-            if (bad != ~0ull) atomicMin(status, bad);
+            words[sw0 + w] = out;
+            if (bad & 0x80u) {
+                // first invalid byte of this word (rare path)
+                for (int c = 0; c < B; ++c) {
+                    const int64_t p = int64_t(w) * B + c;
+                    if (p < slen && lut[ascii[sb0 + p]] == 0xFF) {
+                        atomicMin(status, (unsigned long long)(sb0 + p));
+                        break;
+                    }
+                }
+            }
         }
     }
 }
@@ -110,7 +150,8 @@ void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n,
     launch_status_init(status, s);
     if (n > 0) {
         const int64_t g8 = int64_t(sm_count_current()) * 8;
-        const int grid = int((n + 7) / 8 < g8 ? (n + 7) / 8 : g8);
+        const int64_t need = (n + 63) / 64;  // 8 warps x 8 sequences per block
+        const int grid = int(need < g8 ? need : g8);
         if (fmt == SALOBA_PACK4)
             pack_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
                                                 (unsigned long long*)status);

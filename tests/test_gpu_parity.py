@@ -281,3 +281,26 @@ def test_host_entry_point_matches_device_path(sb):
     s, qe, te, st = sb.align_host(b, sb.BWA_MEM, sb.EXTEND)
     assert st == -1
     assert np.array_equal(s, dev[0]) and np.array_equal(qe, dev[1]) and np.array_equal(te, dev[2])
+
+
+def test_host_context_reuse_offsets_and_errors(sb):
+    b = synth.generate(1, 800, seed=21)
+    dev = gpu_align(sb, b, sb.BWA_MEM, 0)
+    ctx = sb.HostContext(1000, len(b.q_ascii) + 100, len(b.t_ascii) + 100, 300)
+    for _ in range(2):  # reuse
+        s, qe, te, st = sb.align_host(b, sb.BWA_MEM, sb.LOCAL, ctx=ctx)
+        assert st == -1 and np.array_equal(s, dev[0]) and np.array_equal(qe, dev[1]) and np.array_equal(te, dev[2])
+    # a sub-batch whose offsets do not start at 0 (pairs 100..399 of the same buffers)
+    sub = synth.Batch(b.q_ascii, b.q_off[100:401], b.t_ascii, b.t_off[100:401], b.h0[100:400])
+    s, qe, te, st = sb.align_host(sub, sb.BWA_MEM, sb.LOCAL, ctx=ctx)
+    assert st == -1 and np.array_equal(s, dev[0][100:400]) and np.array_equal(te, dev[2][100:400])
+    # an invalid base in pair 523 and an empty target in pair 611 -> status = 523
+    bad = synth.from_pairs([b.pair(k) for k in range(b.n)], b.h0)
+    bad.q_ascii[bad.q_off[523] + 5] = ord("X")
+    s, qe, te, st = sb.align_host(bad, sb.BWA_MEM, sb.LOCAL, ctx=ctx)
+    assert st == 523
+    # capacity exceeded -> SalobaError(EWORKSPACE)
+    big = synth.generate(1, 1200, seed=3)
+    with pytest.raises(sb.SalobaError):
+        sb.align_host(big, sb.BWA_MEM, sb.LOCAL, ctx=ctx)
+    ctx.close()
