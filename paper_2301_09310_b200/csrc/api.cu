@@ -253,7 +253,7 @@ struct saloba_host_ctx {
     void *q = nullptr, *t = nullptr, *qo = nullptr, *to = nullptr, *qw = nullptr, *tw = nullptr, *qwo = nullptr,
          *two = nullptr, *ql = nullptr, *tl = nullptr, *h0 = nullptr, *res = nullptr, *ws = nullptr, *st = nullptr;
     int64_t qwcap = 0, twcap = 0;
-    cudaStream_t copy = nullptr;
+    cudaStream_t copy = nullptr, down = nullptr;
     cudaEvent_t up[HOST_SLICES], done[HOST_SLICES];
     int64_t* hst = nullptr;  // pinned status readback
 };
@@ -273,6 +273,7 @@ SALOBA_API void saloba_host_ctx_destroy(saloba_host_ctx* c) {
         }
         cudaStreamDestroy(c->copy);
     }
+    if (c->down) cudaStreamDestroy(c->down);
     if (c->hst) cudaFreeHost(c->hst);
     cudaSetDevice(prev);
     delete c;
@@ -301,6 +302,7 @@ SALOBA_API saloba_host_ctx* saloba_host_ctx_create(int64_t max_pairs, int64_t ma
               al(&c->h0, max_pairs * 4) && al(&c->res, max_pairs * 12) && al(&c->ws, c->ws_bytes) &&
               al(&c->st, 4 * HOST_SLICES * 8) &&
               cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->down, cudaStreamNonBlocking) == cudaSuccess &&
               cudaMallocHost((void**)&c->hst, 4 * HOST_SLICES * 8) == cudaSuccess;
     if (ok && c->copy)
         for (int i = 0; i < HOST_SLICES; ++i) {
@@ -383,13 +385,14 @@ SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii,
                                 h0d ? h0d + a0 : nullptr, na, sc, mode, SALOBA_PACK4, res + a0, res + n_pairs + a0,
                                 res + 2 * n_pairs + a0, c->ws, c->ws_bytes, st + 4 * i + 2, opt, s);
         cudaEventRecord(c->done[i], s);
-        cudaStreamWaitEvent(c->copy, c->done[i], 0);
-        cudaMemcpyAsync(score + a0, res + a0, na * 4, cudaMemcpyDeviceToHost, c->copy);
-        cudaMemcpyAsync(q_end + a0, res + n_pairs + a0, na * 4, cudaMemcpyDeviceToHost, c->copy);
-        cudaMemcpyAsync(t_end + a0, res + 2 * n_pairs + a0, na * 4, cudaMemcpyDeviceToHost, c->copy);
+        cudaStreamWaitEvent(c->down, c->done[i], 0);
+        cudaMemcpyAsync(score + a0, res + a0, na * 4, cudaMemcpyDeviceToHost, c->down);
+        cudaMemcpyAsync(q_end + a0, res + n_pairs + a0, na * 4, cudaMemcpyDeviceToHost, c->down);
+        cudaMemcpyAsync(t_end + a0, res + 2 * n_pairs + a0, na * 4, cudaMemcpyDeviceToHost, c->down);
     }
-    cudaMemcpyAsync(c->hst, st, sizeof(int64_t) * 4 * nsl, cudaMemcpyDeviceToHost, c->copy);
-    const cudaError_t e = cudaStreamSynchronize(c->copy);
+    cudaMemcpyAsync(c->hst, st, sizeof(int64_t) * 4 * nsl, cudaMemcpyDeviceToHost, c->down);
+    cudaStreamSynchronize(c->copy);
+    const cudaError_t e = cudaStreamSynchronize(c->down);
     cudaStreamSynchronize(s);
     cudaSetDevice(prev);
     if (rc != SALOBA_OK) return rc;
