@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--force-group", type=int, default=0)
     ap.add_argument("--force-path", type=int, default=0)
     ap.add_argument("--keep-order", type=int, default=0)
+    ap.add_argument("--i16-rows", type=int, default=0)
     ap.add_argument("--grouped", action="store_true", help="config 5: components contiguous")
     return ap.parse_args()
 
@@ -228,7 +229,7 @@ def main():
     qo = torch.from_numpy(batch.q_off).to(dev)
     to = torch.from_numpy(batch.t_off).to(dev)
     h0 = torch.from_numpy(batch.h0).to(dev)
-    opts = sb.Options(args.force_group, args.force_path, args.keep_order)
+    opts = sb.Options(args.force_group, args.force_path, args.keep_order, i16_rows=args.i16_rows)
     al = sb.Aligner(n, int(batch.q_off[-1]), int(batch.t_off[-1]), max_q, sb.BWA_MEM, mode, sb.PACK4, opts)
     stream = torch.cuda.current_stream()
     gather_buf = None
@@ -238,7 +239,7 @@ def main():
     bins = torch.zeros(16, dtype=torch.int32, device=dev)
 
     def step(dp_ev=None):
-        o = sb.Options(args.force_group, args.force_path, args.keep_order, dp_ev, bins) if dp_ev else None
+        o = sb.Options(args.force_group, args.force_path, args.keep_order, dp_ev, bins, args.i16_rows) if dp_ev else None
         s, qe, te = al.run(qa, qo, ta, to, h0, options=o)
         if world > 1:  # A5: results gathered to rank 0 (the only collective; none inside the DP)
             dist.gather(al.out[:, :n], gather_buf if rank == 0 else None, dst=0)

@@ -80,7 +80,7 @@ typedef struct {
                              (pairs whose query exceeds that G's spill-row bound keep the scheduler's G) */
     int32_t force_path;   /* 0: auto; 1: int32 exact path for every pair; 2: prefer the int16x2 path */
     int32_t keep_order;   /* 1: do not sort pairs by length (A/B test of the scheduler)            */
-    int32_t reserved0;
+    int32_t i16_rows;     /* 0: default (16); 8: target rows per lane of the int16x2 kernel (A/B knob) */
     void* ev_dp_begin;    /* optional cudaEvent_t recorded on `stream` right before the first DP
                              kernel launch of the call (after packing/scheduling), for profiling */
     void* ev_dp_end;      /* optional cudaEvent_t recorded on `stream` after the last DP kernel   */

@@ -46,7 +46,7 @@ class _Scoring(ctypes.Structure):
 
 class _Options(ctypes.Structure):
     _fields_ = [("force_group", ctypes.c_int32), ("force_path", ctypes.c_int32), ("keep_order", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32), ("ev_dp_begin", ctypes.c_void_p), ("ev_dp_end", ctypes.c_void_p),
+                ("i16_rows", ctypes.c_int32), ("ev_dp_begin", ctypes.c_void_p), ("ev_dp_end", ctypes.c_void_p),
                 ("bin_counts", ctypes.c_void_p), ("reserved", ctypes.c_int32 * 2)]
 
 
@@ -74,9 +74,10 @@ class Options:
     keep_order: int = 0  # 1 = no length sort
     dp_events: tuple | None = None  # (torch.cuda.Event, torch.cuda.Event) bracketing the DP kernels
     bin_counts: torch.Tensor | None = None  # cuda int32[16] <- pairs per bin (path*8 + log2 G)
+    i16_rows: int = 0  # 0 default (16); 8 = 8 target rows per lane in the int16x2 kernel
 
     def _c(self) -> _Options:
-        o = _Options(self.force_group, self.force_path, self.keep_order, 0)
+        o = _Options(self.force_group, self.force_path, self.keep_order, self.i16_rows)
         if self.dp_events is not None:
             o.ev_dp_begin = ctypes.c_void_p(self.dp_events[0].cuda_event)
             o.ev_dp_end = ctypes.c_void_p(self.dp_events[1].cuda_event)

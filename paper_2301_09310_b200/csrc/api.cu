@@ -20,7 +20,7 @@ void launch_status_final(int64_t* st, cudaStream_t s);
 void launch_dp_i32(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s);
 const void* dp_i32_kernel_ptr(int mode, int gidx);
 void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s);
-const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt);
+const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt, int rows);
 void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n, int64_t base, int fmt,
                        uint32_t* words, int64_t* word_off, int32_t* lens, int64_t* status, cudaStream_t s);
 
@@ -30,7 +30,7 @@ struct DevInfo {
     int sms = 0;
     int major = 0;
     int blocks_i32[2][NGROUPS] = {};
-    int blocks_i16[2][NGROUPS] = {};
+    int blocks_i16[2][2][NGROUPS] = {};  // [rows 8|16][mode][gidx]
 };
 static std::mutex g_mu;
 static DevInfo g_dev[64];
@@ -50,9 +50,12 @@ static const DevInfo* dev_info(int device) {
                 int nb = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i32_kernel_ptr(mode, g), BLOCK_THREADS, 0);
                 d.blocks_i32[mode][g] = std::max(1, nb);
-                nb = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i16_kernel_ptr(mode, g, SALOBA_PACK4), I16_THREADS, 0);
-                d.blocks_i16[mode][g] = std::max(1, nb);
+                for (int ri = 0; ri < 2; ++ri) {
+                    nb = 0;
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i16_kernel_ptr(mode, g, SALOBA_PACK4, ri ? 16 : 8),
+                                                                  I16_THREADS, 0);
+                    d.blocks_i16[ri][mode][g] = std::max(1, nb);
+                }
             }
         cudaSetDevice(prev);
         d.init = true;
@@ -74,8 +77,8 @@ struct Layout {
     size_t keys_in, keys_out, vals_in, vals_out, cub, cub_bytes, small, spill, total;
 };
 
-static int grid_for(const DevInfo* d, int mode, int path, int g) {
-    return d->sms * (path == PATH_I16 ? d->blocks_i16[mode][g] : d->blocks_i32[mode][g]);
+static int grid_for(const DevInfo* d, int mode, int path, int g, int rows = 16) {
+    return d->sms * (path == PATH_I16 ? d->blocks_i16[rows == 8 ? 0 : 1][mode][g] : d->blocks_i32[mode][g]);
 }
 static int threads_for(int path) { return path == PATH_I16 ? I16_THREADS : BLOCK_THREADS; }
 // spill rows per subwarp slot: int32 path 2 buffers x (H, F); int16x2 path 4 buffers x (H, F) + selectors
@@ -84,7 +87,8 @@ static int rows_for(int path) { return path == PATH_I16 ? 9 : 4; }
 // bytes of spill pool the bin (mode, path, g) needs when the longest query has Qmax blocks
 static size_t spill_need(const DevInfo* d, int mode, int path, int g, int64_t Qmax) {
     const int64_t G = int64_t(1) << g;
-    const int64_t slots = int64_t(grid_for(d, mode, path, g)) * threads_for(path) / G;
+    const int64_t grid = std::max(grid_for(d, mode, path, g, 8), grid_for(d, mode, path, g, 16));
+    const int64_t slots = grid * threads_for(path) / G;
     const int64_t q = std::min<int64_t>(qmax_for_gidx(g), Qmax);
     const int64_t stride = 8 * q + 8;
     return size_t(slots) * rows_for(path) * size_t(stride) * sizeof(int32_t);
@@ -204,7 +208,8 @@ SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word
     SortKV kv{reinterpret_cast<uint64_t*>(ws + L.keys_in), reinterpret_cast<uint64_t*>(ws + L.keys_out),
               reinterpret_cast<uint32_t*>(ws + L.vals_in), reinterpret_cast<uint32_t*>(ws + L.vals_out),
               ws + L.cub, L.cub_bytes};
-    ClassifyArgs ca{q_words, q_word_off, int(fmt), sc.match, q_len, t_len, h0, n_pairs, int(mode), force_g, o.force_path, o.keep_order, Qsup * 8,
+    const int i16_rows = o.i16_rows == 8 ? 8 : I16_ROWS_DEFAULT;
+    ClassifyArgs ca{q_words, q_word_off, int(fmt), sc.match, q_len, t_len, h0, n_pairs, int(mode), force_g, o.force_path, o.keep_order, i16_rows, Qsup * 8,
                     score, q_end, t_end, kv.keys_in, kv.vals_in, bin_count, (unsigned long long*)status};
     if (run_classify_sort(ca, kv, bin_start, d->sms, s) != cudaSuccess) return SALOBA_ECUDA;
 
@@ -218,13 +223,14 @@ SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word
         a.score = score; a.q_end = q_end; a.t_end = t_end;
         a.perm = kv.vals_out; a.bin_start = bin_start; a.bin_counter = bin_counter;
         a.spill = reinterpret_cast<int32_t*>(ws + L.spill);
+        a.i16_rows = i16_rows;
         if (o.bin_counts) cudaMemcpyAsync(o.bin_counts, bin_count, NBINS * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
         if (o.ev_dp_begin) cudaEventRecord((cudaEvent_t)o.ev_dp_begin, s);
         for (int path = PATH_I16; path >= PATH_I32; --path)
             for (int g = NGROUPS - 1; g >= 0; --g) {
                 a.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(g), Qsup) + 8;
                 if (path == PATH_I16)
-                    launch_dp_i16(int(mode), g, grid_for(d, int(mode), path, g), a, path * 8 + g, s);
+                    launch_dp_i16(int(mode), g, grid_for(d, int(mode), path, g, i16_rows), a, path * 8 + g, s);
                 else
                     launch_dp_i32(int(mode), g, grid_for(d, int(mode), path, g), a, path * 8 + g, s);
             }

@@ -28,6 +28,9 @@ constexpr int MAX_LEN = 1 << 20;   // S:151 overflow envelope for int32 cells
 constexpr int MAX_H0 = 1 << 29;
 constexpr int BLOCK_THREADS = 256;
 constexpr int I16_THREADS = 128;
+// target rows per lane (strip height) of the int16x2 kernel: 16 = two packed target words
+constexpr int I16_ROWS_DEFAULT = 16;
+constexpr int I32_ROWS = 8;
 
 struct SortKV {
     uint64_t* keys_in;
@@ -51,6 +54,7 @@ struct ClassifyArgs {
     int force_gidx;   // -1 = auto
     int force_path;   // 0 auto, 1 int32, 2 int16x2 preferred
     int keep_order;
+    int i16_rows;
     int64_t max_q_supported;  // query length the spill pool was sized for
     int32_t* score;
     int32_t* q_end;
@@ -81,6 +85,7 @@ struct AlignArgs {
     int32_t* bin_counter;     // [NBINS] dynamic work queues
     int32_t* spill;           // pool (int32 view)
     int64_t spill_stride;     // elements per (slot, buffer, H|F) row
+    int32_t i16_rows;         // target rows per lane of the int16x2 kernel (8 or 16)
 };
 
 // 8 consecutive bases [8w, 8w+8) of a packed sequence as 8 nibbles (base c in nibble c).

@@ -95,13 +95,11 @@ struct HalfInfo {
 };
 
 // Top/bottom rows of one chunk.  topX == nullptr: the table boundary (row -1) for half X.
+// Spill rows are interleaved: 16 words per 8-column block, (H0, F0, H1, F1, ..., H7, F7).
 struct ChunkIO {
-    const uint32_t* topA_H;
-    const uint32_t* topA_F;
-    const uint32_t* topB_H;
-    const uint32_t* topB_F;
-    uint32_t* botH;  // nullptr: no spill (last chunk, or pass 2)
-    uint32_t* botF;
+    const uint32_t* topA;  // top row for the low halves (and, outside pass 2, the high halves)
+    const uint32_t* topB;  // pass 2: top row for the high halves
+    uint32_t* bot;         // nullptr: no spill (last chunk, or pass 2)
 };
 
 __device__ __forceinline__ void load8(const uint32_t* p, uint32_t (&v)[8]) {
@@ -113,63 +111,119 @@ __device__ __forceinline__ void load8(const uint32_t* p, uint32_t (&v)[8]) {
 // diagonal candidates D (max H = max(0, max D): any positive H not reached through D is a gap value
 // strictly below an earlier cell).  PASS 2 searches the first cell equal to `target` per half.
 // rowA0 / rowB0: first target row of lane 0 of this chunk in each half (they differ in pass 2).
-template <int G, int MODE, int FMT, bool PASS2>
+// Per-block shared-memory stage for cp.async prefetching (2 slots): selectors per thread, top rows
+// (A and, in pass 2, B checkpoint) per subwarp.
+template <int G>
+struct Stage {
+    uint4 sel[2][2][I16_THREADS];
+    uint4 top[2][I16_THREADS / G][8];
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int G, int R, int MODE, int FMT, bool PASS2>
 __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned mask, const int k, const int Q,
                                               const HalfInfo& A, const HalfInfo& B,
                                               const uint32_t* __restrict__ twA, const uint32_t* __restrict__ twB,
                                               const uint32_t* __restrict__ selbuf, const int rowA0, const int rowB0,
-                                              const ChunkIO io, const uint32_t target, int (&hit)[4]) {
+                                              const ChunkIO io, const uint32_t target, int (&hit)[4], Stage<G>& st,
+                                              const int sub) {
     const int al = a.alpha, be = a.beta;
     const uint32_t nbeta = pack2(-be, -be), nalpha = pack2(-al, -al), noGap = pack2(-al - be, -al - be);
     uint32_t lam = 2;
     while (int(lam) < a.match + 1) lam <<= 1;
-    const int rA = rowA0 + 8 * k, rB = rowB0 + 8 * k;  // my first row in each half
-    uint32_t tabA[8], tabB[8];
-    {
-        const uint32_t ta = (rA < A.m) ? block_codes<FMT>(twA, rA >> 3, A.m) : 0xFFFFFFFFu;
-        const uint32_t tb = (rB < B.m) ? block_codes<FMT>(twB, rB >> 3, B.m) : 0xFFFFFFFFu;
+    const int rA = rowA0 + R * k, rB = rowB0 + R * k;  // my first row in each half (R rows per lane)
+    uint32_t tabA[R], tabB[R];
+#pragma unroll
+    for (int i = 0; i < R / 8; ++i) {
+        const uint32_t ta = (rA + 8 * i < A.m) ? block_codes<FMT>(twA, (rA >> 3) + i, A.m) : 0xFFFFFFFFu;
+        const uint32_t tb = (rB + 8 * i < B.m) ? block_codes<FMT>(twB, (rB >> 3) + i, B.m) : 0xFFFFFFFFu;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            tabA[r] = row_table((ta >> (4 * r)) & 15u, a.match, a.mismatch);
-            tabB[r] = row_table((tb >> (4 * r)) & 15u, a.match, a.mismatch);
+            tabA[8 * i + r] = row_table((ta >> (4 * r)) & 15u, a.match, a.mismatch);
+            tabB[8 * i + r] = row_table((tb >> (4 * r)) & 15u, a.match, a.mismatch);
         }
     }
-    // Hl[r] = H(r, c-1); En[r] = E(r, c) = max(E(r, c-1) - beta, H(r, c-1) - alpha), kept one column
-    // ahead so that H - alpha is consumed immediately.  E(i,0) = max(H(i,-1) - alpha, E(i,-1) - beta);
-    // taking E(i,-1) as "no gap" changes only non-positive E values, which never reach
-    // H = max(0, ...) (clamp neutrality).  Same for F(-1, j) below.
-    uint32_t Hl[8], En[8];
+    // Left boundary of my strip: H(i,-1), and E(i,0) = max(H(i,-1) - alpha, E(i,-1) - beta) with
+    // E(i,-1) taken as "no gap" (only non-positive E values change; they never reach
+    // H = max(0, ...): clamp neutrality; same for F(-1, j)); corner H(r0-1, -1).
+    uint32_t Hl[R], En[R], corner;
+    uint32_t M0 = 0, M1 = 0, M2 = 0, M3 = 0;
+    auto reset_left = [&]() {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const int ha = MODE ? max(0, A.h0 - al - be * (rA + r)) : 0;
-        const int hb = MODE ? max(0, B.h0 - al - be * (rB + r)) : 0;
-        Hl[r] = pack2(ha, hb);
-        En[r] = vadd(Hl[r], nalpha);
-    }
-    uint32_t corner;
-    {
+        for (int r = 0; r < R; ++r) {
+            const int ha = MODE ? max(0, A.h0 - al - be * (rA + r)) : 0;
+            const int hb = MODE ? max(0, B.h0 - al - be * (rB + r)) : 0;
+            Hl[r] = pack2(ha, hb);
+            En[r] = vadd(Hl[r], nalpha);
+        }
         const int ca = MODE ? (rA == 0 ? A.h0 : max(0, A.h0 - al - be * (rA - 1))) : 0;
         const int cb = MODE ? (rB == 0 ? B.h0 : max(0, B.h0 - al - be * (rB - 1))) : 0;
         corner = pack2(ca, cb);
-    }
-    uint32_t M0 = 0, M1 = 0, M2 = 0, M3 = 0;
+        M0 = M1 = M2 = M3 = 0;
+    };
+    reset_left();
+    // my bottom row of the previous step (shuffled to the lane below at the start of each step)
     uint32_t botH[8], botF[8];
 #pragma unroll
     for (int x = 0; x < 8; ++x) botH[x] = botF[x] = 0;
     const int steps = Q + G - 1;
+    // Inputs of step s+1 are fetched during step s with cp.async into a 2-slot shared-memory stage
+    // (no registers held): every lane's 8 selectors, and on lane 0 the spilled top row(s) of its
+    // next block.  Measured (ncu source view) before staging: the lane-0 top-row load was the top
+    // stall of the kernel (~23% of samples), because the whole warp waits for it.
+    const bool topA_mem = io.topA != nullptr;
+    const bool topB_mem = PASS2 && io.topB != io.topA && io.topB != nullptr;
+    auto prefetch = [&](int s2) {
+        const int w2 = s2 - k;
+        if (unsigned(w2) < unsigned(Q)) {
+            cp_async16(&st.sel[s2 & 1][0][threadIdx.x], selbuf + 8 * w2);
+            cp_async16(&st.sel[s2 & 1][1][threadIdx.x], selbuf + 8 * w2 + 4);
+            if (k == 0) {
+                if (topA_mem) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) cp_async16(&st.top[s2 & 1][sub][q], io.topA + 16 * w2 + 4 * q);
+                }
+                if (topB_mem) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) cp_async16(&st.top[s2 & 1][sub][4 + q], io.topB + 16 * w2 + 4 * q);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    prefetch(0);
+    // Every lane takes part in every step's shuffles (warp-uniform loop bounds, full mask); lanes
+    // compute only while 0 <= w < Q.
     for (int s = 0; s < steps; ++s) {
         const int w = s - k;
-        uint32_t topH[8], topF[8];
+        const bool active = unsigned(w) < unsigned(Q);
+        cp_async_wait_all();  // this step's stage (issued during the previous step) has landed
+        prefetch(s + 1);
+        uint32_t topH[8], topF[8], sel[8];
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
             topH[x] = __shfl_up_sync(mask, botH[x], 1, G);
             topF[x] = __shfl_up_sync(mask, botF[x], 1, G);
         }
-        if (k == 0 && w < Q) {
+        {
+            const uint4 s0 = st.sel[s & 1][0][threadIdx.x], s1 = st.sel[s & 1][1][threadIdx.x];
+            sel[0] = s0.x; sel[1] = s0.y; sel[2] = s0.z; sel[3] = s0.w;
+            sel[4] = s1.x; sel[5] = s1.y; sel[6] = s1.z; sel[7] = s1.w;
+        }
+        if (k == 0 && active) {
             // top row of the chunk: spilled row of the previous chunk, or the table boundary
-            if (io.topA_H) {
-                load8(io.topA_H + 8 * w, topH);
-                load8(io.topA_F + 8 * w, topF);
+            if (topA_mem) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 v = st.top[s & 1][sub][q];
+                    topH[2 * q] = v.x; topF[2 * q] = v.y; topH[2 * q + 1] = v.z; topF[2 * q + 1] = v.w;
+                }
             } else {
 #pragma unroll
                 for (int x = 0; x < 8; ++x) {
@@ -178,11 +232,14 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                     topF[x] = noGap;
                 }
             }
-            if (PASS2 && io.topB_H != io.topA_H) {  // high halves from half B's own checkpoint
+            if (PASS2 && io.topB != io.topA) {  // high halves from half B's own checkpoint
                 uint32_t bh[8], bf[8];
-                if (io.topB_H) {
-                    load8(io.topB_H + 8 * w, bh);
-                    load8(io.topB_F + 8 * w, bf);
+                if (topB_mem) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 v = st.top[s & 1][sub][4 + q];
+                        bh[2 * q] = v.x; bf[2 * q] = v.y; bh[2 * q + 1] = v.z; bf[2 * q + 1] = v.w;
+                    }
                 } else {
 #pragma unroll
                     for (int x = 0; x < 8; ++x) {
@@ -198,122 +255,128 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                 }
             }
         }
-        if (unsigned(w) < unsigned(Q)) {
-            uint32_t sel[8];
-            load8(selbuf + 8 * w, sel);
+        if (!active) continue;
 #pragma unroll
-            for (int x = 0; x < 8; ++x) {
-                uint32_t hup = topH[x], fup = topF[x];
-                uint32_t haup = vadd(hup, nalpha);
-                uint32_t hdiag = (x == 0) ? corner : topH[x - 1];
-                uint32_t dprev = 0;
+        for (int x = 0; x < 8; ++x) {
+            uint32_t hup = topH[x], fup = topF[x];
+            uint32_t haup = vadd(hup, nalpha);
+            uint32_t hdiag = (x == 0) ? corner : topH[x - 1];
+            uint32_t dprev = 0;
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const uint32_t f = vaddmax(fup, nbeta, haup);
-                    const uint32_t e = En[r];
-                    const uint32_t sc = prmt(tabA[r], tabB[r], sel[x]);
-                    uint32_t d;
-                    if (MODE) {
-                        // dead-zero (EXTEND): D = hdiag + s if hdiag > 0, else <= 0:
-                        // D = min(hdiag + s, lambda * hdiag), lambda = 2^k >= match + 1.  hdiag >= 0 and
-                        // lambda * hdiag <= 32767 (routing bound), so one 32-bit IMAD scales both halves.
-                        d = vaddmin(hdiag, sc, hdiag * lam);
-                    } else {
-                        d = vadd(hdiag, sc);  // FMA pipe
-                    }
-                    const uint32_t h = vmax3relu(d, e, f);
-                    const uint32_t ha = vadd(h, nalpha);  // FMA pipe
-                    hdiag = Hl[r];
-                    Hl[r] = h;
-                    En[r] = vaddmax(e, nbeta, ha);
-                    hup = h;
-                    haup = ha;
-                    fup = f;
-                    if (!PASS2) {
-                        if (r & 1) {
-                            if (r == 1) M0 = vmax3(M0, dprev, d);
-                            if (r == 3) M1 = vmax3(M1, dprev, d);
-                            if (r == 5) M2 = vmax3(M2, dprev, d);
-                            if (r == 7) M3 = vmax3(M3, dprev, d);
-                        }
-                        dprev = d;
-                    }
+            for (int r = 0; r < R; ++r) {
+                const uint32_t f = vaddmax(fup, nbeta, haup);
+                const uint32_t e = En[r];
+                const uint32_t sc = prmt(tabA[r], tabB[r], sel[x]);
+                uint32_t d;
+                if (MODE) {
+                    // dead-zero (EXTEND): D = hdiag + s if hdiag > 0, else <= 0:
+                    // D = min(hdiag + s, lambda * hdiag), lambda = 2^k >= match + 1.  hdiag >= 0 and
+                    // lambda * hdiag <= 32767 (routing bound), so one 32-bit IMAD scales both halves.
+                    d = vaddmin(hdiag, sc, hdiag * lam);
+                } else {
+                    d = vadd(hdiag, sc);  // FMA pipe
                 }
-                botH[x] = hup;
-                botF[x] = fup;
-                if (PASS2) {
-                    // column maximum; a cell can only equal `target` (the pair maximum) if it is >= it
-                    const uint32_t cm = vmax3(vmax3(Hl[0], Hl[1], Hl[2]), vmax3(Hl[3], Hl[4], Hl[5]), vmax(Hl[6], Hl[7]));
-                    const bool hitA = lo16(cm) >= lo16(target), hitB = hi16(cm) >= hi16(target);
-                    if (hitA || hitB) {
-                        const int col = 8 * w + x;
+                const uint32_t h = vmax3relu(d, e, f);
+                const uint32_t ha = vadd(h, nalpha);  // FMA pipe
+                hdiag = Hl[r];
+                Hl[r] = h;
+                En[r] = vaddmax(e, nbeta, ha);
+                hup = h;
+                haup = ha;
+                fup = f;
+                if (!PASS2) {
+                    if (r & 1) {
+                        if ((r & 7) == 1) M0 = vmax3(M0, dprev, d);
+                        if ((r & 7) == 3) M1 = vmax3(M1, dprev, d);
+                        if ((r & 7) == 5) M2 = vmax3(M2, dprev, d);
+                        if ((r & 7) == 7) M3 = vmax3(M3, dprev, d);
+                    }
+                    dprev = d;
+                }
+            }
+            botH[x] = hup;
+            botF[x] = fup;
+            if (PASS2 && active) {
+                // column maximum; a cell can only equal `target` (the pair maximum) if it is >= it
+                uint32_t cm = vmax3(vmax3(Hl[0], Hl[1], Hl[2]), vmax3(Hl[3], Hl[4], Hl[5]), vmax(Hl[6], Hl[7]));
 #pragma unroll
-                        for (int r = 0; r < 8; ++r) {
-                            if (hitA && lo16(Hl[r]) == lo16(target) && (rA + r < hit[0] || (rA + r == hit[0] && col < hit[1]))) {
-                                hit[0] = rA + r;
-                                hit[1] = col;
-                            }
-                            if (hitB && hi16(Hl[r]) == hi16(target) && (rB + r < hit[2] || (rB + r == hit[2] && col < hit[3]))) {
-                                hit[2] = rB + r;
-                                hit[3] = col;
-                            }
+                for (int r = 8; r < R; r += 2) cm = vmax3(cm, Hl[r], Hl[r + 1]);
+                const bool hitA = lo16(cm) >= lo16(target), hitB = hi16(cm) >= hi16(target);
+                if (hitA || hitB) {
+                    const int col = 8 * w + x;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        if (hitA && lo16(Hl[r]) == lo16(target) && (rA + r < hit[0] || (rA + r == hit[0] && col < hit[1]))) {
+                            hit[0] = rA + r;
+                            hit[1] = col;
+                        }
+                        if (hitB && hi16(Hl[r]) == hi16(target) && (rB + r < hit[2] || (rB + r == hit[2] && col < hit[3]))) {
+                            hit[2] = rB + r;
+                            hit[3] = col;
                         }
                     }
                 }
             }
-            corner = topH[7];
-            if (io.botH && k == G - 1) {
-                uint4* ph = reinterpret_cast<uint4*>(io.botH + 8 * w);
-                uint4* pf = reinterpret_cast<uint4*>(io.botF + 8 * w);
-                ph[0] = make_uint4(botH[0], botH[1], botH[2], botH[3]);
-                ph[1] = make_uint4(botH[4], botH[5], botH[6], botH[7]);
-                pf[0] = make_uint4(botF[0], botF[1], botF[2], botF[3]);
-                pf[1] = make_uint4(botF[4], botF[5], botF[6], botF[7]);
-            }
+        }
+        corner = topH[7];
+        if (io.bot && k == G - 1) {  // chunk-bottom row -> spill (interleaved H, F)
+            uint4* p = reinterpret_cast<uint4*>(io.bot + 16 * w);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) p[q] = make_uint4(botH[2 * q], botF[2 * q], botH[2 * q + 1], botF[2 * q + 1]);
         }
     }
     return vmax(vmax(M0, M1), vmax(M2, M3));
 }
 
-template <int G, int MODE, int FMT>
-__global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bin) {
+template <int G, int R, int MODE, int FMT>
+__global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : 3) dp_i16_kernel(AlignArgs a, int bin) {
+    // Warp-uniform control flow: a warp takes 32/G consecutive work items at once (one atomic),
+    // and runs the warp-maximum of their query blocks and chunk counts; subwarps with a smaller
+    // item compute padding (harmless by the dominance argument above).  Shuffles can then use the
+    // full mask and compile to plain SHFL (no MATCH/convergence bookkeeping).
+    constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int k = lane & (G - 1);
-    const int sub_base = lane & ~(G - 1);
-    const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << sub_base);
     const int64_t slot = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
     const int64_t S = a.spill_stride;
-    // per slot: 4 spill buffers x (H, F) rows, then the query selectors (8 words per block)
+    // per slot: 4 spill buffers (interleaved H,F rows of 2S words), then the query selectors
     uint32_t* const spill = reinterpret_cast<uint32_t*>(a.spill) + slot * 9 * S;
     uint32_t* const selbuf = spill + 8 * S;
+    __shared__ Stage<G> st;
+    const int sub = threadIdx.x / G;  // subwarp index within the block
 
     const int start = a.bin_start[bin];
     const int cnt = a.bin_start[bin + 1] - start;
     const int items = (cnt + 1) >> 1;
 
     for (;;) {
-        int item = 0;
-        if (k == 0) item = atomicAdd(a.bin_counter + bin, 1);
-        item = __shfl_sync(mask, item, 0, G);
-        if (item >= items) break;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(a.bin_counter + bin, 32 / G);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= items) break;
+        const int item = base + lane / G;
+        const bool has = item < items;
         HalfInfo A, B;
-        A.p = int(a.perm[start + 2 * item]);
-        B.p = (2 * item + 1 < cnt) ? int(a.perm[start + 2 * item + 1]) : -1;
-        A.n = a.q_len[A.p];
-        A.m = a.t_len[A.p];
-        A.h0 = MODE ? a.h0[A.p] : 0;
+        A.p = has ? int(a.perm[start + 2 * item]) : -1;
+        B.p = (has && 2 * item + 1 < cnt) ? int(a.perm[start + 2 * item + 1]) : -1;
+        A.n = A.p >= 0 ? a.q_len[A.p] : 0;
+        A.m = A.p >= 0 ? a.t_len[A.p] : 0;
+        A.h0 = (MODE && A.p >= 0) ? a.h0[A.p] : 0;
         B.n = B.p >= 0 ? a.q_len[B.p] : 0;
         B.m = B.p >= 0 ? a.t_len[B.p] : 0;
         B.h0 = (MODE && B.p >= 0) ? a.h0[B.p] : 0;
-        const uint32_t* qwA = a.q_words + a.q_word_off[A.p];
-        const uint32_t* twA = a.t_words + a.t_word_off[A.p];
+        const uint32_t* qwA = A.p >= 0 ? a.q_words + a.q_word_off[A.p] : a.q_words;
+        const uint32_t* twA = A.p >= 0 ? a.t_words + a.t_word_off[A.p] : a.t_words;
         const uint32_t* qwB = B.p >= 0 ? a.q_words + a.q_word_off[B.p] : qwA;
         const uint32_t* twB = B.p >= 0 ? a.t_words + a.t_word_off[B.p] : twA;
-        const int Q = (max(A.n, B.n) + 7) >> 3;
-        const int chunksA = (((A.m + 7) >> 3) + G - 1) / G, chunksB = (((B.m + 7) >> 3) + G - 1) / G;
+        const int Qi = (max(A.n, B.n) + 7) >> 3;
+        const int chunksA = ((A.m + R - 1) / R + G - 1) / G, chunksB = ((B.m + R - 1) / R + G - 1) / G;
         const int chunks = max(chunksA, chunksB);
+        const int Q = int(__reduce_max_sync(FULL, unsigned(Qi)));        // warp-uniform
+        const int chunks_w = int(__reduce_max_sync(FULL, unsigned(chunks)));
 
-        // query selectors, once per work item (shared by every chunk and by pass 2)
+        // query selectors, once per work item (shared by every chunk and by pass 2); blocks past the
+        // item's own length are padding selectors
         for (int w = k; w < Q; w += G) {
             uint32_t sel[8];
             make_selectors(block_codes<FMT>(qwA, w, A.n), block_codes<FMT>(qwB, w, B.n), sel);
@@ -321,7 +384,7 @@ __global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bi
             p[0] = make_uint4(sel[0], sel[1], sel[2], sel[3]);
             p[1] = make_uint4(sel[4], sel[5], sel[6], sel[7]);
         }
-        __syncwarp(mask);
+        __syncwarp(FULL);
 
         // pass 1 -------------------------------------------------------------------------------
         const int floorA = MODE ? A.h0 : 0, floorB = MODE ? B.h0 : 0;
@@ -329,29 +392,29 @@ __global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bi
         int ckA = -1, ckB = -1;               // chunk holding the first maximum (-1: none above floor)
         int bufA = -1, bufB = -1;             // buffer holding that chunk's top row (-1: boundary)
         int rd = -1, wr = 0;
-        for (int c = 0; c < chunks; ++c) {
-            const bool last = (c + 1 == chunks);
+        for (int c = 0; c < chunks_w; ++c) {
+            const bool last = (c + 1 >= chunks);
             ChunkIO io;
-            io.topA_H = io.topB_H = rd >= 0 ? spill + (2 * rd) * S : nullptr;
-            io.topA_F = io.topB_F = rd >= 0 ? spill + (2 * rd + 1) * S : nullptr;
-            io.botH = last ? nullptr : spill + (2 * wr) * S;
-            io.botF = last ? nullptr : spill + (2 * wr + 1) * S;
+            io.topA = io.topB = rd >= 0 ? spill + (2 * rd) * S : nullptr;
+            io.bot = last ? nullptr : spill + (2 * wr) * S;
             int dummy[4];
-            uint32_t m = run_chunk<G, MODE, FMT, false>(a, mask, k, Q, A, B, twA, twB, selbuf, c * 8 * G, c * 8 * G,
-                                                        io, 0u, dummy);
+            uint32_t m = run_chunk<G, R, MODE, FMT, false>(a, FULL, k, Q, A, B, twA, twB, selbuf, c * R * G, c * R * G,
+                                                        io, 0u, dummy, st, sub);
 #pragma unroll
-            for (int off = 1; off < G; off <<= 1) m = vmax(m, __shfl_xor_sync(mask, m, off, G));
-            if (lo16(m) > bestA) {
-                bestA = lo16(m);
-                ckA = c;
-                bufA = rd;
+            for (int off = 1; off < G; off <<= 1) m = vmax(m, __shfl_xor_sync(FULL, m, off, G));
+            if (c < chunks) {
+                if (lo16(m) > bestA) {
+                    bestA = lo16(m);
+                    ckA = c;
+                    bufA = rd;
+                }
+                if (hi16(m) > bestB) {
+                    bestB = hi16(m);
+                    ckB = c;
+                    bufB = rd;
+                }
             }
-            if (hi16(m) > bestB) {
-                bestB = hi16(m);
-                ckB = c;
-                bufB = rd;
-            }
-            __syncwarp(mask);
+            __syncwarp(FULL);
             if (!last) {
                 rd = wr;
                 // next write buffer: not the new read buffer nor a live checkpoint
@@ -362,24 +425,22 @@ __global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bi
         }
         // pass 2 -------------------------------------------------------------------------------
         int hit[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
-        if (ckA >= 0 || ckB >= 0) {
-            const int cA = ckA >= 0 ? ckA : ckB, cB = ckB >= 0 ? ckB : ckA;
-            const int bA = ckA >= 0 ? bufA : bufB, bB = ckB >= 0 ? bufB : bufA;
+        const bool need2 = ckA >= 0 || ckB >= 0;
+        if (__any_sync(FULL, need2)) {
+            const int cA = ckA >= 0 ? ckA : (ckB >= 0 ? ckB : 0), cB = ckB >= 0 ? ckB : cA;
+            const int bA = ckA >= 0 ? bufA : (ckB >= 0 ? bufB : -1), bB = ckB >= 0 ? bufB : bA;
             ChunkIO io;
-            io.topA_H = bA >= 0 ? spill + (2 * bA) * S : nullptr;
-            io.topA_F = bA >= 0 ? spill + (2 * bA + 1) * S : nullptr;
-            io.topB_H = bB >= 0 ? spill + (2 * bB) * S : nullptr;
-            io.topB_F = bB >= 0 ? spill + (2 * bB + 1) * S : nullptr;
-            io.botH = io.botF = nullptr;
-            if (bA == bB && cA != cB) io.topB_H = io.topB_F = nullptr;  // unreachable: distinct chunks own distinct buffers
+            io.topA = bA >= 0 ? spill + (2 * bA) * S : nullptr;
+            io.topB = bB >= 0 ? spill + (2 * bB) * S : nullptr;
+            io.bot = nullptr;
             const uint32_t target = pack2(ckA >= 0 ? bestA : 0x7FFF, ckB >= 0 ? bestB : 0x7FFF);
-            run_chunk<G, MODE, FMT, true>(a, mask, k, Q, A, B, twA, twB, selbuf, cA * 8 * G, cB * 8 * G, io, target,
-                                          hit);
+            run_chunk<G, R, MODE, FMT, true>(a, FULL, k, Q, A, B, twA, twB, selbuf, cA * R * G, cB * R * G, io, target,
+                                             hit, st, sub);
             // first hit in row-major order across the subwarp (rows grow with the lane index)
 #pragma unroll
             for (int off = 1; off < G; off <<= 1) {
-                const int r0 = __shfl_xor_sync(mask, hit[0], off, G), c0 = __shfl_xor_sync(mask, hit[1], off, G);
-                const int r1 = __shfl_xor_sync(mask, hit[2], off, G), c1 = __shfl_xor_sync(mask, hit[3], off, G);
+                const int r0 = __shfl_xor_sync(FULL, hit[0], off, G), c0 = __shfl_xor_sync(FULL, hit[1], off, G);
+                const int r1 = __shfl_xor_sync(FULL, hit[2], off, G), c1 = __shfl_xor_sync(FULL, hit[3], off, G);
                 if (r0 < hit[0] || (r0 == hit[0] && c0 < hit[1])) {
                     hit[0] = r0;
                     hit[1] = c0;
@@ -390,8 +451,8 @@ __global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bi
                 }
             }
         }
-        __syncwarp(mask);
-        if (k == 0) {
+        __syncwarp(FULL);
+        if (k == 0 && A.p >= 0) {
             const int z = MODE ? -1 : 0;
             a.score[A.p] = bestA;
             a.t_end[A.p] = ckA >= 0 ? (hit[0] == INT_MAX ? -3 : hit[0]) : z;
@@ -405,24 +466,28 @@ __global__ void __launch_bounds__(I16_THREADS) dp_i16_kernel(AlignArgs a, int bi
     }
 }
 
-template <int MODE, int FMT>
+template <int MODE, int FMT, int R>
 static const void* kptr16(int gidx) {
     switch (gidx) {
-    case 0: return (const void*)dp_i16_kernel<1, MODE, FMT>;
-    case 1: return (const void*)dp_i16_kernel<2, MODE, FMT>;
-    case 2: return (const void*)dp_i16_kernel<4, MODE, FMT>;
-    case 3: return (const void*)dp_i16_kernel<8, MODE, FMT>;
-    case 4: return (const void*)dp_i16_kernel<16, MODE, FMT>;
-    default: return (const void*)dp_i16_kernel<32, MODE, FMT>;
+    case 0: return (const void*)dp_i16_kernel<1, R, MODE, FMT>;
+    case 1: return (const void*)dp_i16_kernel<2, R, MODE, FMT>;
+    case 2: return (const void*)dp_i16_kernel<4, R, MODE, FMT>;
+    case 3: return (const void*)dp_i16_kernel<8, R, MODE, FMT>;
+    case 4: return (const void*)dp_i16_kernel<16, R, MODE, FMT>;
+    default: return (const void*)dp_i16_kernel<32, R, MODE, FMT>;
     }
 }
-const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt) {
-    if (mode == SALOBA_EXTEND) return fmt == SALOBA_PACK2 ? kptr16<1, 2>(gidx) : kptr16<1, 4>(gidx);
-    return fmt == SALOBA_PACK2 ? kptr16<0, 2>(gidx) : kptr16<0, 4>(gidx);
+template <int R>
+static const void* kptr16_r(int mode, int gidx, int fmt) {
+    if (mode == SALOBA_EXTEND) return fmt == SALOBA_PACK2 ? kptr16<1, 2, R>(gidx) : kptr16<1, 4, R>(gidx);
+    return fmt == SALOBA_PACK2 ? kptr16<0, 2, R>(gidx) : kptr16<0, 4, R>(gidx);
+}
+const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt, int rows) {
+    return rows == 8 ? kptr16_r<8>(mode, gidx, fmt) : kptr16_r<16>(mode, gidx, fmt);
 }
 
 void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s) {
-    const void* fn = dp_i16_kernel_ptr(mode, gidx, a.fmt);
+    const void* fn = dp_i16_kernel_ptr(mode, gidx, a.fmt, a.i16_rows);
     AlignArgs args = a;
     void* params[] = {&args, &bin};
     cudaLaunchKernel(fn, dim3(grid), dim3(I16_THREADS), params, 0, s);

@@ -14,21 +14,24 @@
 namespace saloba {
 
 // modelled lane-steps (one step = one 8x8 block on one lane) + spill cost, for group index g
-__host__ __device__ inline float group_cost(int Q, int strips, int g) {
+// m: target rows; R: rows per lane.  Lane-steps of 8 x R blocks (the Q+G-1 ramp per chunk), a
+// spill term per chunk boundary, and (int16x2) the pass-2 re-run of one chunk.
+__host__ __device__ inline float group_cost(int Q, int m, int g, int R, bool repass) {
     const int G = 1 << g;
+    const int strips = (m + R - 1) / R;
     const int chunks = (strips + G - 1) / G;
-    const float steps = float(chunks) * float(Q + G - 1) * float(G);
+    const float per_chunk = float(Q + G - 1) * float(G) * float(R / 8);
     const float spill = 0.5f * float(chunks - 1) * float(Q);  // write+read of 16 words per block column
-    return steps + spill;
+    return float(chunks) * per_chunk + spill + (repass ? per_chunk : 0.f);
 }
 
-__host__ __device__ inline int choose_gidx(int Q, int strips, int force_gidx, int min_gidx) {
+__host__ __device__ inline int choose_gidx(int Q, int m, int force_gidx, int min_gidx, int R, bool repass) {
     if (force_gidx >= 0 && Q <= qmax_for_gidx(force_gidx)) return force_gidx;
     int best = NGROUPS - 1;
-    float bc = group_cost(Q, strips, best);
+    float bc = group_cost(Q, m, best, R, repass);
     for (int g = NGROUPS - 2; g >= min_gidx; --g) {
         if (Q > qmax_for_gidx(g)) continue;
-        const float c = group_cost(Q, strips, g);
+        const float c = group_cost(Q, m, g, R, repass);
         if (c < bc) {
             bc = c;
             best = g;
@@ -82,9 +85,10 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
             atomicMin(a.status, (unsigned long long)k);
             key = (uint64_t(bin) << 56) | uint64_t(k);
         } else {
-            const int Q = (n + 7) >> 3, strips = (m + 7) >> 3;
+            const int Q = (n + 7) >> 3;
             const int path = (a.force_path != 1 && i16_eligible(a, k, n, m)) ? PATH_I16 : PATH_I32;
-            const int g = choose_gidx(Q, strips, a.force_gidx, 0);
+            const int g = path == PATH_I16 ? choose_gidx(Q, m, a.force_gidx, 1, a.i16_rows, true)
+                                           : choose_gidx(Q, m, a.force_gidx, 0, I32_ROWS, false);
             bin = path * 8 + g;
             if (a.keep_order)
                 key = (uint64_t(bin) << 56) | uint64_t(k);
