@@ -81,8 +81,8 @@ static int grid_for(const DevInfo* d, int mode, int path, int g, int rows = 16) 
     return d->sms * (path == PATH_I16 ? d->blocks_i16[rows == 8 ? 0 : 1][mode][g] : d->blocks_i32[mode][g]);
 }
 static int threads_for(int path) { return path == PATH_I16 ? I16_THREADS : BLOCK_THREADS; }
-// spill rows per subwarp slot: int32 path 2 buffers x (H, F); int16x2 path 4 buffers x (H, F) + selectors
-static int rows_for(int path) { return path == PATH_I16 ? 9 : 4; }
+// spill rows per subwarp slot: int32 path 2 buffers x (H, F); int16x2 path 4 interleaved (H, F) buffers
+static int rows_for(int path) { return path == PATH_I16 ? 8 : 4; }
 
 // bytes of spill pool the bin (mode, path, g) needs when the longest query has Qmax blocks
 static size_t spill_need(const DevInfo* d, int mode, int path, int g, int64_t Qmax) {

@@ -111,12 +111,14 @@ __device__ __forceinline__ void load8(const uint32_t* p, uint32_t (&v)[8]) {
 // diagonal candidates D (max H = max(0, max D): any positive H not reached through D is a gap value
 // strictly below an earlier cell).  PASS 2 searches the first cell equal to `target` per half.
 // rowA0 / rowB0: first target row of lane 0 of this chunk in each half (they differ in pass 2).
-// Per-block shared-memory stage for cp.async prefetching (2 slots): selectors per thread, top rows
-// (A and, in pass 2, B checkpoint) per subwarp.
+// Per-block shared-memory stage for cp.async prefetching, STAGE_DEPTH slots (inputs of step s are
+// requested during step s - STAGE_DEPTH + 1): the two packed query words of each lane's block, and
+// per subwarp the spilled top row(s) of lane 0 (A and, in pass 2, B checkpoint).
+constexpr int STAGE_DEPTH = 3;
 template <int G>
 struct Stage {
-    uint4 sel[2][2][I16_THREADS];
-    uint4 top[2][I16_THREADS / G][8];
+    uint32_t q[STAGE_DEPTH][2][I16_THREADS];
+    uint4 top[STAGE_DEPTH][I16_THREADS / G][4];
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -124,13 +126,37 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// nibble codes of block w from a staged packed word (FMT 4: the word; FMT 2: half of word w/2),
+// with positions >= len as padding 15 (same contract as block_codes)
+template <int FMT>
+__device__ __forceinline__ uint32_t staged_codes(uint32_t word, int w, int len) {
+    const int valid = len - 8 * w;
+    if (valid <= 0) return 0xFFFFFFFFu;
+    uint32_t x = word;
+    if (FMT == SALOBA_PACK2) {
+        const uint32_t h = word >> ((w & 1) * 16);
+        x = 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x |= ((h >> (2 * c)) & 3u) << (4 * c);
+    }
+    if (valid < 8) x |= 0xFFFFFFFFu << (4 * valid);
+    return x;
+}
 
 template <int G, int R, int MODE, int FMT, bool PASS2>
 __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned mask, const int k, const int Q,
                                               const HalfInfo& A, const HalfInfo& B,
                                               const uint32_t* __restrict__ twA, const uint32_t* __restrict__ twB,
-                                              const uint32_t* __restrict__ selbuf, const int rowA0, const int rowB0,
+                                              const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
+                                              const int rowA0, const int rowB0,
                                               const ChunkIO io, const uint32_t target, int (&hit)[4], Stage<G>& st,
                                               const int sub) {
     const int al = a.alpha, be = a.beta;
@@ -179,49 +205,46 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
     // stall of the kernel (~23% of samples), because the whole warp waits for it.
     const bool topA_mem = io.topA != nullptr;
     const bool topB_mem = PASS2 && io.topB != io.topA && io.topB != nullptr;
-    auto prefetch = [&](int s2) {
+    auto prefetch = [&](int s2, int slot) {
         const int w2 = s2 - k;
         if (unsigned(w2) < unsigned(Q)) {
-            cp_async16(&st.sel[s2 & 1][0][threadIdx.x], selbuf + 8 * w2);
-            cp_async16(&st.sel[s2 & 1][1][threadIdx.x], selbuf + 8 * w2 + 4);
+            const int wi = FMT == SALOBA_PACK2 ? (w2 >> 1) : w2;
+            if (8 * w2 < A.n) cp_async4(&st.q[slot][0][threadIdx.x], qwA + wi);
+            if (8 * w2 < B.n) cp_async4(&st.q[slot][1][threadIdx.x], qwB + wi);
             if (k == 0) {
                 if (topA_mem) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) cp_async16(&st.top[s2 & 1][sub][q], io.topA + 16 * w2 + 4 * q);
+                    for (int q = 0; q < 4; ++q) cp_async16(&st.top[slot][sub][q], io.topA + 16 * w2 + 4 * q);
                 }
-                if (topB_mem) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) cp_async16(&st.top[s2 & 1][sub][4 + q], io.topB + 16 * w2 + 4 * q);
-                }
+
             }
         }
         cp_async_commit();
     };
-    prefetch(0);
+    prefetch(0, 0);
+    prefetch(1, 1);
+    int cur = 0;  // stage slot of step s (s % STAGE_DEPTH)
     // Every lane takes part in every step's shuffles (warp-uniform loop bounds, full mask); lanes
     // compute only while 0 <= w < Q.
     for (int s = 0; s < steps; ++s) {
         const int w = s - k;
         const bool active = unsigned(w) < unsigned(Q);
-        cp_async_wait_all();  // this step's stage (issued during the previous step) has landed
-        prefetch(s + 1);
+        cp_async_wait<STAGE_DEPTH - 2>();  // this step's stage (issued two steps ago) has landed
+        prefetch(s + 2, cur == 0 ? 2 : cur - 1);
         uint32_t topH[8], topF[8], sel[8];
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
             topH[x] = __shfl_up_sync(mask, botH[x], 1, G);
             topF[x] = __shfl_up_sync(mask, botF[x], 1, G);
         }
-        {
-            const uint4 s0 = st.sel[s & 1][0][threadIdx.x], s1 = st.sel[s & 1][1][threadIdx.x];
-            sel[0] = s0.x; sel[1] = s0.y; sel[2] = s0.z; sel[3] = s0.w;
-            sel[4] = s1.x; sel[5] = s1.y; sel[6] = s1.z; sel[7] = s1.w;
-        }
+        make_selectors(staged_codes<FMT>(st.q[cur][0][threadIdx.x], w, A.n),
+                       staged_codes<FMT>(st.q[cur][1][threadIdx.x], w, B.n), sel);
         if (k == 0 && active) {
             // top row of the chunk: spilled row of the previous chunk, or the table boundary
             if (topA_mem) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const uint4 v = st.top[s & 1][sub][q];
+                    const uint4 v = st.top[cur][sub][q];
                     topH[2 * q] = v.x; topF[2 * q] = v.y; topH[2 * q + 1] = v.z; topF[2 * q + 1] = v.w;
                 }
             } else {
@@ -234,10 +257,10 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
             }
             if (PASS2 && io.topB != io.topA) {  // high halves from half B's own checkpoint
                 uint32_t bh[8], bf[8];
-                if (topB_mem) {
+                if (topB_mem) {  // pass 2 only: not staged
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint4 v = st.top[s & 1][sub][4 + q];
+                        const uint4 v = reinterpret_cast<const uint4*>(io.topB + 16 * w)[q];
                         bh[2 * q] = v.x; bf[2 * q] = v.y; bh[2 * q + 1] = v.z; bf[2 * q + 1] = v.w;
                     }
                 } else {
@@ -255,6 +278,9 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                 }
             }
         }
+        const int cur_now = cur;
+        cur = (cur == STAGE_DEPTH - 1) ? 0 : cur + 1;
+        (void)cur_now;
         if (!active) continue;
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
@@ -339,9 +365,8 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : 3) dp_i16_kernel(Ali
     const int k = lane & (G - 1);
     const int64_t slot = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
     const int64_t S = a.spill_stride;
-    // per slot: 4 spill buffers (interleaved H,F rows of 2S words), then the query selectors
-    uint32_t* const spill = reinterpret_cast<uint32_t*>(a.spill) + slot * 9 * S;
-    uint32_t* const selbuf = spill + 8 * S;
+    // per slot: 4 spill buffers (interleaved H,F rows of 2S words)
+    uint32_t* const spill = reinterpret_cast<uint32_t*>(a.spill) + slot * 8 * S;
     __shared__ Stage<G> st;
     const int sub = threadIdx.x / G;  // subwarp index within the block
 
@@ -375,16 +400,6 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : 3) dp_i16_kernel(Ali
         const int Q = int(__reduce_max_sync(FULL, unsigned(Qi)));        // warp-uniform
         const int chunks_w = int(__reduce_max_sync(FULL, unsigned(chunks)));
 
-        // query selectors, once per work item (shared by every chunk and by pass 2); blocks past the
-        // item's own length are padding selectors
-        for (int w = k; w < Q; w += G) {
-            uint32_t sel[8];
-            make_selectors(block_codes<FMT>(qwA, w, A.n), block_codes<FMT>(qwB, w, B.n), sel);
-            uint4* p = reinterpret_cast<uint4*>(selbuf + 8 * w);
-            p[0] = make_uint4(sel[0], sel[1], sel[2], sel[3]);
-            p[1] = make_uint4(sel[4], sel[5], sel[6], sel[7]);
-        }
-        __syncwarp(FULL);
 
         // pass 1 -------------------------------------------------------------------------------
         const int floorA = MODE ? A.h0 : 0, floorB = MODE ? B.h0 : 0;
@@ -398,7 +413,7 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : 3) dp_i16_kernel(Ali
             io.topA = io.topB = rd >= 0 ? spill + (2 * rd) * S : nullptr;
             io.bot = last ? nullptr : spill + (2 * wr) * S;
             int dummy[4];
-            uint32_t m = run_chunk<G, R, MODE, FMT, false>(a, FULL, k, Q, A, B, twA, twB, selbuf, c * R * G, c * R * G,
+            uint32_t m = run_chunk<G, R, MODE, FMT, false>(a, FULL, k, Q, A, B, twA, twB, qwA, qwB, c * R * G, c * R * G,
                                                         io, 0u, dummy, st, sub);
 #pragma unroll
             for (int off = 1; off < G; off <<= 1) m = vmax(m, __shfl_xor_sync(FULL, m, off, G));
@@ -434,7 +449,7 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : 3) dp_i16_kernel(Ali
             io.topB = bB >= 0 ? spill + (2 * bB) * S : nullptr;
             io.bot = nullptr;
             const uint32_t target = pack2(ckA >= 0 ? bestA : 0x7FFF, ckB >= 0 ? bestB : 0x7FFF);
-            run_chunk<G, R, MODE, FMT, true>(a, FULL, k, Q, A, B, twA, twB, selbuf, cA * R * G, cB * R * G, io, target,
+            run_chunk<G, R, MODE, FMT, true>(a, FULL, k, Q, A, B, twA, twB, qwA, qwB, cA * R * G, cB * R * G, io, target,
                                              hit, st, sub);
             // first hit in row-major order across the subwarp (rows grow with the lane index)
 #pragma unroll

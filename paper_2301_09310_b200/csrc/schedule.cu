@@ -21,7 +21,7 @@ __host__ __device__ inline float group_cost(int Q, int m, int g, int R, bool rep
     const int strips = (m + R - 1) / R;
     const int chunks = (strips + G - 1) / G;
     const float per_chunk = float(Q + G - 1) * float(G) * float(R / 8);
-    const float spill = 0.5f * float(chunks - 1) * float(Q);  // write+read of 16 words per block column
+    const float spill = 0.1f * float(chunks - 1) * float(Q);  // write+read of 16 words per block column
     return float(chunks) * per_chunk + spill + (repass ? per_chunk : 0.f);
 }
 
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
         } else {
             const int Q = (n + 7) >> 3;
             const int path = (a.force_path != 1 && i16_eligible(a, k, n, m)) ? PATH_I16 : PATH_I32;
-            const int g = path == PATH_I16 ? choose_gidx(Q, m, a.force_gidx, 1, a.i16_rows, true)
+            const int g = path == PATH_I16 ? choose_gidx(Q, m, a.force_gidx, 0, a.i16_rows, true)
                                            : choose_gidx(Q, m, a.force_gidx, 0, I32_ROWS, false);
             bin = path * 8 + g;
             if (a.keep_order)
