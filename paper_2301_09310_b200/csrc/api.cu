@@ -31,7 +31,10 @@ struct DevInfo {
     int major = 0;
     int blocks_i32[2][NGROUPS] = {};
     int blocks_i16[2][2][NGROUPS] = {};  // [rows 8|16][mode][gidx]
+    int max_blocks_per_sm = 1;           // max resident blocks of any DP kernel (block-slot pool)
+    cudaStream_t aux[4] = {};            // bins run as concurrent kernels on these
 };
+constexpr int NAUX = 4;
 static std::mutex g_mu;
 static DevInfo g_dev[64];
 
@@ -57,6 +60,12 @@ static const DevInfo* dev_info(int device) {
                     d.blocks_i16[ri][mode][g] = std::max(1, nb);
                 }
             }
+        for (int mode = 0; mode < 2; ++mode)
+            for (int g = 0; g < NGROUPS; ++g) {
+                d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_i32[mode][g]);
+                for (int ri = 0; ri < 2; ++ri) d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_i16[ri][mode][g]);
+            }
+        for (int i = 0; i < NAUX; ++i) cudaStreamCreateWithFlags(&d.aux[i], cudaStreamNonBlocking);
         cudaSetDevice(prev);
         d.init = true;
     }
@@ -84,22 +93,21 @@ static int threads_for(int path) { return path == PATH_I16 ? I16_THREADS : BLOCK
 // spill rows per subwarp slot: int32 path 2 buffers x (H, F); int16x2 path 4 interleaved (H, F) buffers
 static int rows_for(int path) { return path == PATH_I16 ? 8 : 4; }
 
-// bytes of spill pool the bin (mode, path, g) needs when the longest query has Qmax blocks
-static size_t spill_need(const DevInfo* d, int mode, int path, int g, int64_t Qmax) {
+// spill words one resident block of bin (path, g) needs when the longest query has Qmax blocks
+static int64_t block_need_words(int path, int g, int64_t Qmax) {
     const int64_t G = int64_t(1) << g;
-    const int64_t grid = std::max(grid_for(d, mode, path, g, 8), grid_for(d, mode, path, g, 16));
-    const int64_t slots = grid * threads_for(path) / G;
     const int64_t q = std::min<int64_t>(qmax_for_gidx(g), Qmax);
-    const int64_t stride = 8 * q + 8;
-    return size_t(slots) * rows_for(path) * size_t(stride) * sizeof(int32_t);
+    return int64_t(threads_for(path)) / G * rows_for(path) * (8 * q + 8);
 }
-
+static int64_t block_slot_words(int64_t Qmax) {
+    int64_t w = 0;
+    for (int g = 0; g < NGROUPS; ++g)
+        for (int path = 0; path < 2; ++path) w = std::max(w, block_need_words(path, g, Qmax));
+    return (w + 63) / 64 * 64;
+}
+static int block_slots(const DevInfo* d) { return (d->sms * d->max_blocks_per_sm + 32 + 31) / 32 * 32; }  // whole bitmap words
 static size_t spill_pool_bytes(const DevInfo* d, int64_t Qmax) {
-    size_t need = 0;
-    for (int mode = 0; mode < 2; ++mode)
-        for (int g = 0; g < NGROUPS; ++g)
-            for (int path = 0; path < 2; ++path) need = std::max(need, spill_need(d, mode, path, g, Qmax));
-    return need;
+    return size_t(block_slots(d)) * size_t(block_slot_words(Qmax)) * sizeof(int32_t);
 }
 
 static Layout layout(int64_t n, size_t spill_bytes) {
@@ -223,17 +231,36 @@ SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word
         a.score = score; a.q_end = q_end; a.t_end = t_end;
         a.perm = kv.vals_out; a.bin_start = bin_start; a.bin_counter = bin_counter;
         a.spill = reinterpret_cast<int32_t*>(ws + L.spill);
+        a.block_slot_words = block_slot_words(Qsup);
+        a.slot_bitmap = reinterpret_cast<uint32_t*>(small + 96);
+        a.slot_words = (block_slots(d) + 31) / 32;
         a.i16_rows = i16_rows;
         if (o.bin_counts) cudaMemcpyAsync(o.bin_counts, bin_count, NBINS * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
         if (o.ev_dp_begin) cudaEventRecord((cudaEvent_t)o.ev_dp_begin, s);
+        // All bins run as concurrent kernels (fork/join over the device's auxiliary streams), longest
+        // bins first: a few long pairs then overlap the bulk of short ones instead of leaving most SMs
+        // idle in a tail (§III-A load imbalance).  Blocks without work exit at once.
+        cudaEvent_t fork = nullptr, join[NAUX] = {};
+        cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+        cudaEventRecord(fork, s);
+        for (int i = 0; i < NAUX; ++i) cudaStreamWaitEvent(d->aux[i], fork, 0);
+        int j = 0;
         for (int path = PATH_I16; path >= PATH_I32; --path)
-            for (int g = NGROUPS - 1; g >= 0; --g) {
+            for (int g = NGROUPS - 1; g >= 0; --g, ++j) {
+                cudaStream_t as = d->aux[j % NAUX];
                 a.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(g), Qsup) + 8;
                 if (path == PATH_I16)
-                    launch_dp_i16(int(mode), g, grid_for(d, int(mode), path, g, i16_rows), a, path * 8 + g, s);
+                    launch_dp_i16(int(mode), g, grid_for(d, int(mode), path, g, i16_rows), a, path * 8 + g, as);
                 else
-                    launch_dp_i32(int(mode), g, grid_for(d, int(mode), path, g), a, path * 8 + g, s);
+                    launch_dp_i32(int(mode), g, grid_for(d, int(mode), path, g), a, path * 8 + g, as);
             }
+        for (int i = 0; i < NAUX; ++i) {
+            cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming);
+            cudaEventRecord(join[i], d->aux[i]);
+            cudaStreamWaitEvent(s, join[i], 0);
+            cudaEventDestroy(join[i]);
+        }
+        cudaEventDestroy(fork);
         if (o.ev_dp_end) cudaEventRecord((cudaEvent_t)o.ev_dp_end, s);
     }
     launch_status_final(status, s);

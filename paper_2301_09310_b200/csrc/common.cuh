@@ -22,7 +22,7 @@ constexpr int NGROUPS = 6;
 // Largest query block count Q = ceil(qlen/8) a bin of group size G accepts: bounds the spill pool
 // (one chunk-boundary row per subwarp slot).  G = 32 takes everything up to the batch maximum.
 __host__ __device__ constexpr int qmax_for_gidx(int gidx) {
-    return gidx == 0 ? 40 : gidx == 1 ? 80 : gidx == 2 ? 160 : gidx == 3 ? 320 : gidx == 4 ? 1280 : (1 << 17);
+    return gidx == 0 ? 80 : gidx == 1 ? 160 : gidx == 2 ? 320 : gidx == 3 ? 640 : gidx == 4 ? 1280 : (1 << 17);
 }
 constexpr int MAX_LEN = 1 << 20;   // S:151 overflow envelope for int32 cells
 constexpr int MAX_H0 = 1 << 29;
@@ -83,8 +83,11 @@ struct AlignArgs {
     const uint32_t* perm;     // sorted position -> input index
     const int32_t* bin_start; // [NBINS + 1]
     int32_t* bin_counter;     // [NBINS] dynamic work queues
-    int32_t* spill;           // pool (int32 view)
-    int64_t spill_stride;     // elements per (slot, buffer, H|F) row
+    int32_t* spill;           // pool (int32 view), cut into block slots of block_slot_words
+    int64_t spill_stride;     // elements per (subwarp slot, buffer, H|F) row
+    int64_t block_slot_words; // pool words per resident block
+    uint32_t* slot_bitmap;    // one bit per block slot: set while a resident block owns it
+    int32_t slot_words;       // 32-bit words in slot_bitmap
     int32_t i16_rows;         // target rows per lane of the int16x2 kernel (8 or 16)
 };
 
@@ -102,5 +105,36 @@ __device__ __forceinline__ uint32_t load_block8(const uint32_t* __restrict__ wor
 }
 
 __device__ __forceinline__ int nib(uint32_t w, int c) { return (w >> (4 * c)) & 15; }
+
+// Block-slot allocator for the spill pool.  Bins run as concurrent kernels, so slots are owned by
+// RESIDENT blocks rather than indexed by blockIdx: the pool holds (SMs x max resident blocks per SM)
+// block slots, a resident block claims a free bit at start and releases it at exit.  A free bit
+// always exists because at most that many blocks can be resident at once.
+__device__ __forceinline__ int acquire_block_slot(uint32_t* bitmap, int words) {
+    __shared__ int s_slot;
+    if (threadIdx.x == 0) {
+        int got = -1;
+        for (int it = 0; got < 0; ++it) {
+            const int w = int((blockIdx.x + it) % unsigned(words));
+            uint32_t cur = *((volatile uint32_t*)bitmap + w);
+            while (cur != 0xFFFFFFFFu) {
+                const int b = __ffs(~cur) - 1;
+                const uint32_t old = atomicOr(bitmap + w, 1u << b);
+                if (!(old & (1u << b))) {
+                    got = w * 32 + b;
+                    break;
+                }
+                cur = old | (1u << b);
+            }
+        }
+        s_slot = got;
+    }
+    __syncthreads();
+    return s_slot;
+}
+__device__ __forceinline__ void release_block_slot(uint32_t* bitmap, int slot) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAnd(bitmap + (slot >> 5), ~(1u << (slot & 31)));
+}
 
 }  // namespace saloba

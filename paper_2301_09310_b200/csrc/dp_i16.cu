@@ -363,10 +363,10 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : 3) dp_i16_kernel(Ali
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int k = lane & (G - 1);
-    const int64_t slot = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
     const int64_t S = a.spill_stride;
-    // per slot: 4 spill buffers (interleaved H,F rows of 2S words)
-    uint32_t* const spill = reinterpret_cast<uint32_t*>(a.spill) + slot * 8 * S;
+    // per subwarp: 4 spill buffers (interleaved H,F rows of 2S words) inside this block's pool slot
+    const int bslot = acquire_block_slot(a.slot_bitmap, a.slot_words);
+    uint32_t* const spill = reinterpret_cast<uint32_t*>(a.spill) + bslot * a.block_slot_words + (threadIdx.x / G) * 8 * S;
     __shared__ Stage<G> st;
     const int sub = threadIdx.x / G;  // subwarp index within the block
 
@@ -479,6 +479,7 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : 3) dp_i16_kernel(Ali
             }
         }
     }
+    release_block_slot(a.slot_bitmap, bslot);
 }
 
 template <int MODE, int FMT, int R>

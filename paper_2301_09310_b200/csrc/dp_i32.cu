@@ -27,8 +27,8 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
     const int k = lane & (G - 1);
     const int sub_base = lane & ~(G - 1);
     const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << sub_base);
-    const int64_t slot = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
-    int32_t* const spill = a.spill + slot * 4 * a.spill_stride;
+    const int bslot = acquire_block_slot(a.slot_bitmap, a.slot_words);
+    int32_t* const spill = a.spill + bslot * a.block_slot_words + (threadIdx.x / G) * 4 * a.spill_stride;
 
     const int start = a.bin_start[bin];
     const int cnt = a.bin_start[bin + 1] - start;
@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
             a.t_end[p] = besti;
         }
     }
+    release_block_slot(a.slot_bitmap, bslot);
 }
 
 template <int MODE>
