@@ -2,6 +2,8 @@
 // host-buffer end-to-end entry point.  No compute happens here; every step runs in kernels.
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -401,13 +403,27 @@ SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii,
         count_launches(2);
     }
     int rc = SALOBA_OK;
+    // optional timeline (SALOBA_TRACE=1): upload-done / compute-start / compute-end per slice
+    static const bool trace = getenv("SALOBA_TRACE") != nullptr;
+    cudaEvent_t tr0 = nullptr, tup[HOST_SLICES] = {}, tcs[HOST_SLICES] = {}, tce[HOST_SLICES] = {};
+    if (trace) {
+        cudaEventCreate(&tr0);
+        cudaEventRecord(tr0, c->copy);
+        for (int i = 0; i < nsl; ++i) {
+            cudaEventCreate(&tup[i]);
+            cudaEventCreate(&tcs[i]);
+            cudaEventCreate(&tce[i]);
+        }
+    }
     for (int i = 0; i < nsl && rc == SALOBA_OK; ++i) {
         const int64_t a0 = cut[i], a1 = cut[i + 1], na = a1 - a0;
         const int64_t qs = q_off[a0] - qb0, qe = q_off[a1] - qb0, ts = t_off[a0] - tb0, te = t_off[a1] - tb0;
         cudaMemcpyAsync(qd + qs, q_ascii + q_off[a0], qe - qs, cudaMemcpyHostToDevice, c->copy);
         cudaMemcpyAsync(td + ts, t_ascii + t_off[a0], te - ts, cudaMemcpyHostToDevice, c->copy);
         cudaEventRecord(c->up[i], c->copy);
+        if (trace) cudaEventRecord(tup[i], c->copy);
         cudaStreamWaitEvent(s, c->up[i], 0);
+        if (trace) cudaEventRecord(tcs[i], s);
         launch_pack_range(qd, qo + a0, na, a0, SALOBA_PACK4, static_cast<uint32_t*>(c->qw),
                           static_cast<int64_t*>(c->qwo) + a0, static_cast<int32_t*>(c->ql) + a0, st + 4 * i + 0, s);
         launch_pack_range(td, to + a0, na, a0, SALOBA_PACK4, static_cast<uint32_t*>(c->tw),
@@ -418,6 +434,7 @@ SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii,
                                 h0d ? h0d + a0 : nullptr, na, sc, mode, SALOBA_PACK4, res + a0, res + n_pairs + a0,
                                 res + 2 * n_pairs + a0, c->ws, c->ws_bytes, st + 4 * i + 2, opt, s);
         cudaEventRecord(c->done[i], s);
+        if (trace) cudaEventRecord(tce[i], s);
         cudaStreamWaitEvent(c->down, c->done[i], 0);
         cudaMemcpyAsync(score + a0, res + a0, na * 4, cudaMemcpyDeviceToHost, c->down);
         cudaMemcpyAsync(q_end + a0, res + n_pairs + a0, na * 4, cudaMemcpyDeviceToHost, c->down);
@@ -426,6 +443,20 @@ SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii,
     cudaMemcpyAsync(c->hst, st, sizeof(int64_t) * 4 * nsl, cudaMemcpyDeviceToHost, c->down);
     cudaStreamSynchronize(c->copy);
     const cudaError_t e = cudaStreamSynchronize(c->down);
+    if (trace) {
+        cudaStreamSynchronize(s);
+        for (int i = 0; i < nsl; ++i) {
+            float u = 0, cs = 0, ce = 0;
+            cudaEventElapsedTime(&u, tr0, tup[i]);
+            cudaEventElapsedTime(&cs, tr0, tcs[i]);
+            cudaEventElapsedTime(&ce, tr0, tce[i]);
+            fprintf(stderr, "[saloba trace] slice %d: upload done %.3f ms, compute %.3f -> %.3f ms\n", i, u, cs, ce);
+            cudaEventDestroy(tup[i]);
+            cudaEventDestroy(tcs[i]);
+            cudaEventDestroy(tce[i]);
+        }
+        cudaEventDestroy(tr0);
+    }
     cudaStreamSynchronize(s);
     cudaSetDevice(prev);
     if (rc != SALOBA_OK) return rc;

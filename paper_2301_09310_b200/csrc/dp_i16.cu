@@ -94,6 +94,19 @@ struct HalfInfo {
     int n, m, h0, p;  // p < 0: dummy half
 };
 
+// raw packed target words of a lane's R-row strip starting at rows rA / rB (no use of the loaded
+// values here, so the loads stay in flight until run_chunk consumes them)
+template <int R, int FMT>
+__device__ __forceinline__ void load_target_raw(const HalfInfo& A, const HalfInfo& B, const uint32_t* twA,
+                                                const uint32_t* twB, int rA, int rB, uint32_t (&raw)[R / 4]) {
+#pragma unroll
+    for (int i = 0; i < R / 8; ++i) {
+        const int ba = (rA >> 3) + i, bb = (rB >> 3) + i;
+        raw[i] = (8 * ba < A.m) ? __ldg(twA + (FMT == SALOBA_PACK2 ? (ba >> 1) : ba)) : 0u;
+        raw[R / 8 + i] = (8 * bb < B.m) ? __ldg(twB + (FMT == SALOBA_PACK2 ? (bb >> 1) : bb)) : 0u;
+    }
+}
+
 // Top/bottom rows of one chunk.  topX == nullptr: the table boundary (row -1) for half X.
 // Spill rows are interleaved: 16 words per 8-column block, (H0, F0, H1, F1, ..., H7, F7).
 struct ChunkIO {
@@ -158,7 +171,7 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                                               const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
                                               const int rowA0, const int rowB0,
                                               const ChunkIO io, const uint32_t target, int (&hit)[4], Stage<G>& st,
-                                              const int sub) {
+                                              const int sub, const uint32_t (&twraw)[R / 4]) {
     const int al = a.alpha, be = a.beta;
     const uint32_t nbeta = pack2(-be, -be), nalpha = pack2(-al, -al), noGap = pack2(-al - be, -al - be);
     uint32_t lam = 2;
@@ -167,8 +180,9 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
     uint32_t tabA[R], tabB[R];
 #pragma unroll
     for (int i = 0; i < R / 8; ++i) {
-        const uint32_t ta = (rA + 8 * i < A.m) ? block_codes<FMT>(twA, (rA >> 3) + i, A.m) : 0xFFFFFFFFu;
-        const uint32_t tb = (rB + 8 * i < B.m) ? block_codes<FMT>(twB, (rB >> 3) + i, B.m) : 0xFFFFFFFFu;
+        // twraw: raw target words of my strip, loaded by the caller one chunk ahead
+        const uint32_t ta = staged_codes<FMT>(twraw[i], (rA >> 3) + i, A.m);
+        const uint32_t tb = staged_codes<FMT>(twraw[R / 8 + i], (rB >> 3) + i, B.m);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             tabA[8 * i + r] = row_table((ta >> (4 * r)) & 15u, a.match, a.mismatch);
@@ -221,16 +235,16 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
         }
         cp_async_commit();
     };
-    prefetch(0, 0);
-    prefetch(1, 1);
+#pragma unroll
+    for (int p = 0; p < STAGE_DEPTH - 1; ++p) prefetch(p, p);
     int cur = 0;  // stage slot of step s (s % STAGE_DEPTH)
     // Every lane takes part in every step's shuffles (warp-uniform loop bounds, full mask); lanes
     // compute only while 0 <= w < Q.
     for (int s = 0; s < steps; ++s) {
         const int w = s - k;
         const bool active = unsigned(w) < unsigned(Q);
-        cp_async_wait<STAGE_DEPTH - 2>();  // this step's stage (issued two steps ago) has landed
-        prefetch(s + 2, cur == 0 ? 2 : cur - 1);
+        cp_async_wait<STAGE_DEPTH - 2>();  // this step's stage (issued STAGE_DEPTH-1 steps ago) has landed
+        prefetch(s + STAGE_DEPTH - 1, cur == 0 ? STAGE_DEPTH - 1 : cur - 1);
         uint32_t topH[8], topF[8], sel[8];
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
@@ -407,14 +421,21 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : 3) dp_i16_kernel(Ali
         int ckA = -1, ckB = -1;               // chunk holding the first maximum (-1: none above floor)
         int bufA = -1, bufB = -1;             // buffer holding that chunk's top row (-1: boundary)
         int rd = -1, wr = 0;
+        uint32_t twn[R / 4];
+        load_target_raw<R, FMT>(A, B, twA, twB, R * k, R * k, twn);
         for (int c = 0; c < chunks_w; ++c) {
+            uint32_t twc[R / 4];
+#pragma unroll
+            for (int i = 0; i < R / 4; ++i) twc[i] = twn[i];
+            if (c + 1 < chunks_w)
+                load_target_raw<R, FMT>(A, B, twA, twB, (c + 1) * R * G + R * k, (c + 1) * R * G + R * k, twn);
             const bool last = (c + 1 >= chunks);
             ChunkIO io;
             io.topA = io.topB = rd >= 0 ? spill + (2 * rd) * S : nullptr;
             io.bot = last ? nullptr : spill + (2 * wr) * S;
             int dummy[4];
             uint32_t m = run_chunk<G, R, MODE, FMT, false>(a, FULL, k, Q, A, B, twA, twB, qwA, qwB, c * R * G, c * R * G,
-                                                        io, 0u, dummy, st, sub);
+                                                        io, 0u, dummy, st, sub, twc);
 #pragma unroll
             for (int off = 1; off < G; off <<= 1) m = vmax(m, __shfl_xor_sync(FULL, m, off, G));
             if (c < chunks) {
@@ -449,8 +470,10 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : 3) dp_i16_kernel(Ali
             io.topB = bB >= 0 ? spill + (2 * bB) * S : nullptr;
             io.bot = nullptr;
             const uint32_t target = pack2(ckA >= 0 ? bestA : 0x7FFF, ckB >= 0 ? bestB : 0x7FFF);
+            uint32_t tw2[R / 4];
+            load_target_raw<R, FMT>(A, B, twA, twB, cA * R * G + R * k, cB * R * G + R * k, tw2);
             run_chunk<G, R, MODE, FMT, true>(a, FULL, k, Q, A, B, twA, twB, qwA, qwB, cA * R * G, cB * R * G, io, target,
-                                             hit, st, sub);
+                                             hit, st, sub, tw2);
             // first hit in row-major order across the subwarp (rows grow with the lane index)
 #pragma unroll
             for (int off = 1; off < G; off <<= 1) {
