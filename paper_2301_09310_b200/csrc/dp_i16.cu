@@ -128,6 +128,9 @@ __device__ __forceinline__ void load8(const uint32_t* p, uint32_t (&v)[8]) {
 // requested during step s - STAGE_DEPTH + 1): the two packed query words of each lane's block, and
 // per subwarp the spilled top row(s) of lane 0 (A and, in pass 2, B checkpoint).
 constexpr int STAGE_DEPTH = 3;
+#ifndef I16_MINB16
+#define I16_MINB16 3
+#endif
 template <int G>
 struct Stage {
     uint32_t q[STAGE_DEPTH][2][I16_THREADS];
@@ -369,7 +372,7 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
 }
 
 template <int G, int R, int MODE, int FMT>
-__global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : 3) dp_i16_kernel(AlignArgs a, int bin) {
+__global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : I16_MINB16) dp_i16_kernel(AlignArgs a, int bin) {
     // Warp-uniform control flow: a warp takes 32/G consecutive work items at once (one atomic),
     // and runs the warp-maximum of their query blocks and chunk counts; subwarps with a smaller
     // item compute padding (harmless by the dominance argument above).  Shuffles can then use the
