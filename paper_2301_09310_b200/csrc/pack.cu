@@ -45,16 +45,17 @@ __device__ __forceinline__ uint2 load8(const uint8_t* __restrict__ base, int64_t
     return make_uint2(lo, hi);
 }
 
-// One warp packs a tile of up to 8 consecutive sequences: lanes sweep the tile's words (flattened
-// across sequence boundaries) so short sequences do not leave lanes idle.  Per base: one byte
-// extract (ALU), one shared-memory table lookup (MIO) and one shift-accumulate.
+// A warp packs a tile of 32 consecutive sequences: lane i reads sequence i's offsets, a warp scan
+// gives each sequence's first flattened word, and the lanes then sweep the tile's words (flattened
+// across sequence boundaries, located by a 5-step shuffle binary search) so that short sequences
+// leave no lane idle and every iteration has 32 independent 8-byte loads in flight.
 template <int BITS>
 __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ ascii, const int64_t* __restrict__ byte_off,
                                                    int64_t n_seqs, int64_t base, uint32_t* __restrict__ words,
                                                    int64_t* __restrict__ word_off, int32_t* __restrict__ lens,
                                                    unsigned long long* __restrict__ status) {
     constexpr int B = 32 / BITS;  // bases per word
-    constexpr int SPT = 8;        // sequences per warp tile
+    constexpr unsigned FULL = 0xffffffffu;
     __shared__ uint8_t lut[256];
     build_lut(lut, BITS);
     __syncthreads();
@@ -62,12 +63,11 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ a
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     const int64_t total = byte_off[n_seqs];  // ascii is readable up to here
-    for (int64_t s0 = warp * SPT; s0 < n_seqs; s0 += nwarps * SPT) {
-        // lanes 0..SPT-1 describe one sequence each
+    for (int64_t s0 = warp * 32; s0 < n_seqs; s0 += nwarps * 32) {
+        const int64_t s = s0 + lane;
         int64_t b0 = 0, len = 0, w0 = 0;
         int nw = 0;
-        const int64_t s = s0 + lane;
-        if (lane < SPT && s < n_seqs) {
+        if (s < n_seqs) {
             b0 = byte_off[s];
             len = byte_off[s + 1] - b0;
             w0 = b0 / B + s + base;
@@ -76,25 +76,28 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ a
             if (lens) lens[s] = int32_t(len);
             if (s == n_seqs - 1) word_off[n_seqs] = byte_off[n_seqs] / B + n_seqs + base;
         }
-        // inclusive scan of word counts over the tile
-        int incl = nw;
+        int incl = nw;  // inclusive scan of word counts
 #pragma unroll
-        for (int off = 1; off < SPT; off <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, off);
             if (lane >= off) incl += v;
         }
-        const int tile_words = __shfl_sync(0xffffffffu, incl, SPT - 1);
-        for (int fb = 0; fb < tile_words; fb += 32) {  // all lanes iterate: shuffles stay converged
+        const int excl = incl - nw;
+        const int tile_words = __shfl_sync(FULL, incl, 31);
+        for (int fb = 0; fb < tile_words; fb += 32) {
             const int f = fb + lane;
-            // sequence i of the tile holding flattened word f
+            // largest i with excl_i <= f (binary search over the lanes' exclusive offsets)
             int i = 0;
 #pragma unroll
-            for (int j = 0; j < SPT - 1; ++j) i += (f >= __shfl_sync(0xffffffffu, incl, j)) ? 1 : 0;
-            if (i > SPT - 1) i = SPT - 1;
-            const int start = __shfl_sync(0xffffffffu, incl - nw, i);
-            const int64_t sb0 = __shfl_sync(0xffffffffu, b0, i);
-            const int64_t slen = __shfl_sync(0xffffffffu, len, i);
-            const int64_t sw0 = __shfl_sync(0xffffffffu, w0, i);
+            for (int step = 16; step >= 1; step >>= 1) {
+                const int cand = i + step;
+                const int e = __shfl_sync(FULL, excl, cand & 31);
+                if (cand < 32 && e <= f) i = cand;
+            }
+            const int start = __shfl_sync(FULL, excl, i);
+            const int64_t sb0 = __shfl_sync(FULL, b0, i);
+            const int64_t slen = __shfl_sync(FULL, len, i);
+            const int64_t sw0 = __shfl_sync(FULL, w0, i);
             if (f >= tile_words) continue;
             const int w = f - start;
             uint32_t out = 0, bad = 0;
@@ -102,13 +105,13 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ a
             for (int half = 0; half < B / 8; ++half) {
                 const int64_t p0 = int64_t(w) * B + half * 8;
                 const uint2 by = load8(ascii, sb0 + p0, total);
+                const int nvalid = int(slen - p0 < 8 ? slen - p0 : 8);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     const uint32_t byte = ((c < 4 ? by.x : by.y) >> (8 * (c & 3))) & 0xFFu;
                     uint32_t code = lut[byte];
-                    const bool valid = p0 + c < slen;
-                    if (valid) bad |= code;
-                    if (!valid || code == 0xFFu) code = BITS == 4 ? 15u : 0u;  // padding / invalid
+                    if (c < nvalid) bad |= code;
+                    if (c >= nvalid || code == 0xFFu) code = BITS == 4 ? 15u : 0u;  // padding / invalid
                     out |= code << (BITS * (half * 8 + c));
                 }
             }
@@ -150,7 +153,7 @@ void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n,
     launch_status_init(status, s);
     if (n > 0) {
         const int64_t g8 = int64_t(sm_count_current()) * 8;
-        const int64_t need = (n + 63) / 64;  // 8 warps x 8 sequences per block
+        const int64_t need = (n + 255) / 256;  // 8 warps per block, 32 sequences per warp
         const int grid = int(need < g8 ? need : g8);
         if (fmt == SALOBA_PACK4)
             pack_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
