@@ -173,12 +173,13 @@ static int gidx_of(int G) {
     }
 }
 
-SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word_off, const int32_t* q_len,
-                                  const uint32_t* t_words, const int64_t* t_word_off, const int32_t* t_len,
-                                  const int32_t* h0, int64_t n_pairs, saloba_scoring sc, saloba_mode mode,
-                                  saloba_packing fmt, int32_t* score, int32_t* q_end, int32_t* t_end,
-                                  void* workspace, size_t workspace_bytes, int64_t* status,
-                                  const saloba_options* opt, void* stream) {
+// aux: NAUX streams the bins fork onto (nullptr: the device's shared set)
+static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, const int32_t* q_len,
+                            const uint32_t* t_words, const int64_t* t_word_off, const int32_t* t_len,
+                            const int32_t* h0, int64_t n_pairs, saloba_scoring sc, saloba_mode mode,
+                            saloba_packing fmt, int32_t* score, int32_t* q_end, int32_t* t_end, void* workspace,
+                            size_t workspace_bytes, int64_t* status, const saloba_options* opt, void* stream,
+                            const cudaStream_t* aux_in) {
     if (n_pairs < 0 || n_pairs > int64_t(INT32_MAX) - 1024) return SALOBA_EINVAL;
     if (!status || !workspace) return SALOBA_EINVAL;
     if (n_pairs > 0 && (!q_words || !q_word_off || !q_len || !t_words || !t_word_off || !t_len || !score ||
@@ -245,11 +246,12 @@ SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word
         cudaEvent_t fork = nullptr, join[NAUX] = {};
         cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
         cudaEventRecord(fork, s);
-        for (int i = 0; i < NAUX; ++i) cudaStreamWaitEvent(d->aux[i], fork, 0);
+        const cudaStream_t* aux = aux_in ? aux_in : d->aux;
+        for (int i = 0; i < NAUX; ++i) cudaStreamWaitEvent(aux[i], fork, 0);
         int j = 0;
         for (int path = PATH_I16; path >= PATH_I32; --path)
             for (int g = NGROUPS - 1; g >= 0; --g, ++j) {
-                cudaStream_t as = d->aux[j % NAUX];
+                cudaStream_t as = aux[j % NAUX];
                 a.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(g), Qsup) + 8;
                 if (path == PATH_I16)
                     launch_dp_i16(int(mode), g, grid_for(d, int(mode), path, g, i16_rows), a, path * 8 + g, as);
@@ -258,7 +260,7 @@ SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word
             }
         for (int i = 0; i < NAUX; ++i) {
             cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming);
-            cudaEventRecord(join[i], d->aux[i]);
+            cudaEventRecord(join[i], aux[i]);
             cudaStreamWaitEvent(s, join[i], 0);
             cudaEventDestroy(join[i]);
         }
@@ -267,6 +269,16 @@ SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word
     }
     launch_status_final(status, s);
     return cudaGetLastError() == cudaSuccess ? SALOBA_OK : SALOBA_ECUDA;
+}
+
+SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word_off, const int32_t* q_len,
+                                  const uint32_t* t_words, const int64_t* t_word_off, const int32_t* t_len,
+                                  const int32_t* h0, int64_t n_pairs, saloba_scoring sc, saloba_mode mode,
+                                  saloba_packing fmt, int32_t* score, int32_t* q_end, int32_t* t_end,
+                                  void* workspace, size_t workspace_bytes, int64_t* status,
+                                  const saloba_options* opt, void* stream) {
+    return align_batch_impl(q_words, q_word_off, q_len, t_words, t_word_off, t_len, h0, n_pairs, sc, mode, fmt, score,
+                            q_end, t_end, workspace, workspace_bytes, status, opt, stream, nullptr);
 }
 
 // ---- end-to-end from host buffers -----------------------------------------------------------
@@ -286,7 +298,13 @@ struct saloba_host_ctx {
     int64_t slice_pairs = 0;
     size_t ws_bytes = 0;
     void *q = nullptr, *t = nullptr, *qo = nullptr, *to = nullptr, *qw = nullptr, *tw = nullptr, *qwo = nullptr,
-         *two = nullptr, *ql = nullptr, *tl = nullptr, *h0 = nullptr, *res = nullptr, *ws = nullptr, *st = nullptr;
+         *two = nullptr, *ql = nullptr, *tl = nullptr, *h0 = nullptr, *res = nullptr, *st = nullptr;
+    // two compute pipelines (workspace + stream + auxiliary streams) so that slice i+1 packs and
+    // aligns while slice i drains
+    void* ws[2] = {nullptr, nullptr};
+    cudaStream_t cs[2] = {nullptr, nullptr};
+    cudaStream_t aux[2][4] = {};
+    cudaEvent_t fork = nullptr, pjoin[2] = {nullptr, nullptr};
     int64_t qwcap = 0, twcap = 0;
     cudaStream_t copy = nullptr, down = nullptr;
     cudaEvent_t up[HOST_SLICES], done[HOST_SLICES];
@@ -298,9 +316,16 @@ SALOBA_API void saloba_host_ctx_destroy(saloba_host_ctx* c) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
-    void* bufs[] = {c->q, c->t, c->qo, c->to, c->qw, c->tw, c->qwo, c->two, c->ql, c->tl, c->h0, c->res, c->ws, c->st};
+    void* bufs[] = {c->q, c->t, c->qo, c->to, c->qw, c->tw, c->qwo, c->two, c->ql, c->tl, c->h0, c->res, c->ws[0], c->ws[1], c->st};
     for (void* b : bufs)
         if (b) cudaFree(b);
+    for (int p = 0; p < 2; ++p) {
+        if (c->cs[p]) cudaStreamDestroy(c->cs[p]);
+        for (int i = 0; i < 4; ++i)
+            if (c->aux[p][i]) cudaStreamDestroy(c->aux[p][i]);
+        if (c->pjoin[p]) cudaEventDestroy(c->pjoin[p]);
+    }
+    if (c->fork) cudaEventDestroy(c->fork);
     if (c->copy) {
         for (int i = 0; i < HOST_SLICES; ++i) {
             cudaEventDestroy(c->up[i]);
@@ -334,16 +359,24 @@ SALOBA_API saloba_host_ctx* saloba_host_ctx_create(int64_t max_pairs, int64_t ma
     bool ok = c->ws_bytes > 0 && al(&c->q, max_q_bytes) && al(&c->t, max_t_bytes) && al(&c->qo, np1 * 8) &&
               al(&c->to, np1 * 8) && al(&c->qw, c->qwcap * 4) && al(&c->tw, c->twcap * 4) && al(&c->qwo, np1 * 8) &&
               al(&c->two, np1 * 8) && al(&c->ql, max_pairs * 4) && al(&c->tl, max_pairs * 4) &&
-              al(&c->h0, max_pairs * 4) && al(&c->res, max_pairs * 12) && al(&c->ws, c->ws_bytes) &&
+              al(&c->h0, max_pairs * 4) && al(&c->res, max_pairs * 12) && al(&c->ws[0], c->ws_bytes) &&
+              al(&c->ws[1], c->ws_bytes) &&
               al(&c->st, 4 * HOST_SLICES * 8) &&
               cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamCreateWithFlags(&c->down, cudaStreamNonBlocking) == cudaSuccess &&
               cudaMallocHost((void**)&c->hst, 4 * HOST_SLICES * 8) == cudaSuccess;
-    if (ok && c->copy)
+    if (ok && c->copy) {
         for (int i = 0; i < HOST_SLICES; ++i) {
             cudaEventCreateWithFlags(&c->up[i], cudaEventDisableTiming);
             cudaEventCreateWithFlags(&c->done[i], cudaEventDisableTiming);
         }
+        for (int p = 0; p < 2; ++p) {
+            cudaStreamCreateWithFlags(&c->cs[p], cudaStreamNonBlocking);
+            for (int i = 0; i < 4; ++i) cudaStreamCreateWithFlags(&c->aux[p][i], cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&c->pjoin[p], cudaEventDisableTiming);
+        }
+        cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+    }
     cudaSetDevice(prev);
     if (!ok) {
         saloba_host_ctx_destroy(c);
@@ -393,6 +426,10 @@ SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii,
     int32_t* res = static_cast<int32_t*>(c->res);
     int32_t* h0d = h0 ? static_cast<int32_t*>(c->h0) : nullptr;
 
+    // the two compute pipelines start after everything already queued on the caller's stream
+    cudaEventRecord(c->fork, s);
+    cudaStreamWaitEvent(c->cs[0], c->fork, 0);
+    cudaStreamWaitEvent(c->cs[1], c->fork, 0);
     // offsets (8 B per pair) and h0 first; rebased on the device so the host never touches them
     cudaMemcpyAsync(qo, q_off, (n_pairs + 1) * 8, cudaMemcpyHostToDevice, c->copy);
     cudaMemcpyAsync(to, t_off, (n_pairs + 1) * 8, cudaMemcpyHostToDevice, c->copy);
@@ -422,25 +459,31 @@ SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii,
         cudaMemcpyAsync(td + ts, t_ascii + t_off[a0], te - ts, cudaMemcpyHostToDevice, c->copy);
         cudaEventRecord(c->up[i], c->copy);
         if (trace) cudaEventRecord(tup[i], c->copy);
-        cudaStreamWaitEvent(s, c->up[i], 0);
-        if (trace) cudaEventRecord(tcs[i], s);
+        const int pp = i & 1;
+        cudaStream_t ps = c->cs[pp];
+        cudaStreamWaitEvent(ps, c->up[i], 0);
+        if (trace) cudaEventRecord(tcs[i], ps);
         launch_pack_range(qd, qo + a0, na, a0, SALOBA_PACK4, static_cast<uint32_t*>(c->qw),
-                          static_cast<int64_t*>(c->qwo) + a0, static_cast<int32_t*>(c->ql) + a0, st + 4 * i + 0, s);
+                          static_cast<int64_t*>(c->qwo) + a0, static_cast<int32_t*>(c->ql) + a0, st + 4 * i + 0, ps);
         launch_pack_range(td, to + a0, na, a0, SALOBA_PACK4, static_cast<uint32_t*>(c->tw),
-                          static_cast<int64_t*>(c->two) + a0, static_cast<int32_t*>(c->tl) + a0, st + 4 * i + 1, s);
-        rc = saloba_align_batch(static_cast<uint32_t*>(c->qw), static_cast<int64_t*>(c->qwo) + a0,
-                                static_cast<int32_t*>(c->ql) + a0, static_cast<uint32_t*>(c->tw),
-                                static_cast<int64_t*>(c->two) + a0, static_cast<int32_t*>(c->tl) + a0,
-                                h0d ? h0d + a0 : nullptr, na, sc, mode, SALOBA_PACK4, res + a0, res + n_pairs + a0,
-                                res + 2 * n_pairs + a0, c->ws, c->ws_bytes, st + 4 * i + 2, opt, s);
-        cudaEventRecord(c->done[i], s);
-        if (trace) cudaEventRecord(tce[i], s);
+                          static_cast<int64_t*>(c->two) + a0, static_cast<int32_t*>(c->tl) + a0, st + 4 * i + 1, ps);
+        rc = align_batch_impl(static_cast<uint32_t*>(c->qw), static_cast<int64_t*>(c->qwo) + a0,
+                              static_cast<int32_t*>(c->ql) + a0, static_cast<uint32_t*>(c->tw),
+                              static_cast<int64_t*>(c->two) + a0, static_cast<int32_t*>(c->tl) + a0,
+                              h0d ? h0d + a0 : nullptr, na, sc, mode, SALOBA_PACK4, res + a0, res + n_pairs + a0,
+                              res + 2 * n_pairs + a0, c->ws[pp], c->ws_bytes, st + 4 * i + 2, opt, ps, c->aux[pp]);
+        cudaEventRecord(c->done[i], ps);
+        if (trace) cudaEventRecord(tce[i], ps);
         cudaStreamWaitEvent(c->down, c->done[i], 0);
         cudaMemcpyAsync(score + a0, res + a0, na * 4, cudaMemcpyDeviceToHost, c->down);
         cudaMemcpyAsync(q_end + a0, res + n_pairs + a0, na * 4, cudaMemcpyDeviceToHost, c->down);
         cudaMemcpyAsync(t_end + a0, res + 2 * n_pairs + a0, na * 4, cudaMemcpyDeviceToHost, c->down);
     }
     cudaMemcpyAsync(c->hst, st, sizeof(int64_t) * 4 * nsl, cudaMemcpyDeviceToHost, c->down);
+    for (int p = 0; p < 2; ++p) {  // the caller's stream resumes after both pipelines
+        cudaEventRecord(c->pjoin[p], c->cs[p]);
+        cudaStreamWaitEvent(s, c->pjoin[p], 0);
+    }
     cudaStreamSynchronize(c->copy);
     const cudaError_t e = cudaStreamSynchronize(c->down);
     if (trace) {
