@@ -27,10 +27,10 @@ __host__ __device__ inline float group_cost(int Q, int m, int g, int R, bool rep
 
 __host__ __device__ inline int choose_gidx(int Q, int m, int force_gidx, int min_gidx, int R, bool repass) {
     if (force_gidx >= 0 && Q <= qmax_for_gidx(force_gidx)) return force_gidx;
-    // long queries: every chunk boundary row is Q*64 B; with many resident subwarps these rows no
-    // longer fit in L2 and spill traffic goes to HBM.  Measured on config 4 (B200, round 1):
-    // G=32 5.2, G=16 4.8, G=8 3.8 TCUPS, so long queries take G=32 outright.
-    if (Q >= 256) return NGROUPS - 1;
+    // long queries: every chunk-boundary row is Q*64 B, and with many resident subwarps the rows no
+    // longer fit in L2.  Measured on config 4 (B200, round 1): G=16 6.1 TCUPS at 100k pairs, G=8
+    // 3.8, G=4 3.4 -> long queries take G >= 16 (the cost model picks 16 or 32).
+    if (Q >= 256) min_gidx = 4;
     int best = NGROUPS - 1;
     float bc = group_cost(Q, m, best, R, repass);
     for (int g = NGROUPS - 2; g >= min_gidx; --g) {
