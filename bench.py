@@ -321,8 +321,15 @@ def main():
     path = "int16x2" if n16 >= n32 else "int32"
     peak = sms * f_mhz * 1e6 * p_int / OPS_PER_CELL[path] / 1e9
     achieved = cells_rank / (dp_ms_avg * 1e-3) / 1e9
+    traffic = None
+    try:  # DRAM bytes per launch of the dominant kernel from the committed ncu capture of this command
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_dp_traffic.json")))
+        if tj.get("workload") == f"config{cfg}" and tj.get("pairs") == n and args.mode == "local":
+            traffic = tj["traffic_bytes_per_launch"]
+    except Exception:
+        pass
     roof = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GCUPS",
-            "frac": round(achieved / peak, 4), "traffic": None,
+            "frac": round(achieved / peak, 4), "traffic": traffic,
             "kernel": ("dp_i16_kernel" if path == "int16x2" else "dp_i32_kernel") +
                       " (all bins of one call, CUDA events on the launching stream)",
             "bins": {f"{'i16' if b >= 8 else 'i32'}_G{1 << (b % 8)}": c for b, c in enumerate(bc) if c and b != 15},

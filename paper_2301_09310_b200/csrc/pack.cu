@@ -45,87 +45,90 @@ __device__ __forceinline__ uint2 load8(const uint8_t* __restrict__ base, int64_t
     return make_uint2(lo, hi);
 }
 
-// A warp packs a tile of 32 consecutive sequences: lane i reads sequence i's offsets, a warp scan
-// gives each sequence's first flattened word, and the lanes then sweep the tile's words (flattened
-// across sequence boundaries, located by a 5-step shuffle binary search) so that short sequences
-// leave no lane idle and every iteration has 32 independent 8-byte loads in flight.
+// 8 ASCII bases -> 8 nibble codes, fast path: if all 8 are A/C/G/T (either case) the codes come
+// from bit arithmetic (A 0x41 -> 0, C 0x43 -> 1, G 0x47 -> 2, T 0x54 -> 3: ((u>>1)&3) ^ ((u>>2)&1))
+// and a whole-word compare against the re-synthesised canonical letters proves every byte valid.
+// Returns false (caller takes the table path) for U, N, invalid bytes.
+__device__ __forceinline__ bool fast_acgt8(uint2 by, uint32_t& out) {
+    uint32_t nib[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t u = (h ? by.y : by.x) & 0xDFDFDFDFu;                   // upper case
+        const uint32_t code = ((u >> 1) ^ ((u >> 2) & 0x01010101u)) & 0x03030303u;
+        const uint32_t t = code | (code >> 4);
+        uint32_t sel, canon;
+        asm("prmt.b32 %0, %1, 0, 0x4420;" : "=r"(sel) : "r"(t));              // 4 codes as nibbles
+        asm("prmt.b32 %0, %1, 0, %2;" : "=r"(canon) : "r"(0x54474341u), "r"(sel));  // "ACGT"[code]
+        if (canon != u) return false;
+        nib[h] = sel & 0xFFFFu;
+    }
+    out = nib[0] | (nib[1] << 16);
+    return true;
+}
+
+// A warp packs a tile of 32 consecutive sequences, one lane per sequence: lane i walks its own
+// sequence word by word (8-byte loads, L1-served across the lane's consecutive iterations) — no
+// per-word bookkeeping.  Common words take the bit-arithmetic path above; words with U, N, padding
+// or invalid bytes take the shared-memory byte->code table.
 template <int BITS>
 __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ ascii, const int64_t* __restrict__ byte_off,
                                                    int64_t n_seqs, int64_t base, uint32_t* __restrict__ words,
                                                    int64_t* __restrict__ word_off, int32_t* __restrict__ lens,
                                                    unsigned long long* __restrict__ status) {
     constexpr int B = 32 / BITS;  // bases per word
-    constexpr unsigned FULL = 0xffffffffu;
     __shared__ uint8_t lut[256];
     build_lut(lut, BITS);
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     const int64_t total = byte_off[n_seqs];  // ascii is readable up to here
-    for (int64_t s0 = warp * 32; s0 < n_seqs; s0 += nwarps * 32) {
-        const int64_t s = s0 + lane;
-        int64_t b0 = 0, len = 0, w0 = 0;
-        int nw = 0;
-        if (s < n_seqs) {
-            b0 = byte_off[s];
-            len = byte_off[s + 1] - b0;
-            w0 = b0 / B + s + base;
-            nw = int((len + B - 1) / B);
-            word_off[s] = w0;
-            if (lens) lens[s] = int32_t(len);
-            if (s == n_seqs - 1) word_off[n_seqs] = byte_off[n_seqs] / B + n_seqs + base;
-        }
-        int incl = nw;  // inclusive scan of word counts
+    for (int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < n_seqs; s += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b0 = byte_off[s], len = byte_off[s + 1] - b0;
+        const int64_t w0 = b0 / B + s + base;
+        word_off[s] = w0;
+        if (lens) lens[s] = int32_t(len);
+        if (s == n_seqs - 1) word_off[n_seqs] = byte_off[n_seqs] / B + n_seqs + base;
+        const int nw = int((len + B - 1) / B);
+        constexpr int U = 4;  // words in flight per lane (memory-level parallelism)
+        for (int wb = 0; wb < nw; wb += U) {
+          uint2 pre[U];
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int v = __shfl_up_sync(FULL, incl, off);
-            if (lane >= off) incl += v;
-        }
-        const int excl = incl - nw;
-        const int tile_words = __shfl_sync(FULL, incl, 31);
-        for (int fb = 0; fb < tile_words; fb += 32) {
-            const int f = fb + lane;
-            // largest i with excl_i <= f (binary search over the lanes' exclusive offsets)
-            int i = 0;
+          for (int u = 0; u < U; ++u)
+              pre[u] = (BITS == 4 && wb + u < nw) ? load8(ascii, b0 + int64_t(wb + u) * B, total) : make_uint2(0, 0);
 #pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-                const int cand = i + step;
-                const int e = __shfl_sync(FULL, excl, cand & 31);
-                if (cand < 32 && e <= f) i = cand;
-            }
-            const int start = __shfl_sync(FULL, excl, i);
-            const int64_t sb0 = __shfl_sync(FULL, b0, i);
-            const int64_t slen = __shfl_sync(FULL, len, i);
-            const int64_t sw0 = __shfl_sync(FULL, w0, i);
-            if (f >= tile_words) continue;
-            const int w = f - start;
+          for (int u = 0; u < U; ++u) {
+            const int w = wb + u;
+            if (w >= nw) break;
             uint32_t out = 0, bad = 0;
+            bool fast = false;
+            if (BITS == 4 && len - int64_t(w) * B >= 8) fast = fast_acgt8(pre[u], out);
+            if (!fast) {
+                out = 0;
 #pragma unroll
-            for (int half = 0; half < B / 8; ++half) {
-                const int64_t p0 = int64_t(w) * B + half * 8;
-                const uint2 by = load8(ascii, sb0 + p0, total);
-                const int nvalid = int(slen - p0 < 8 ? slen - p0 : 8);
+                for (int half = 0; half < B / 8; ++half) {
+                    const int64_t p0 = int64_t(w) * B + half * 8;
+                    const uint2 by = load8(ascii, b0 + p0, total);
+                    const int nvalid = int(len - p0 < 8 ? len - p0 : 8);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const uint32_t byte = ((c < 4 ? by.x : by.y) >> (8 * (c & 3))) & 0xFFu;
-                    uint32_t code = lut[byte];
-                    if (c < nvalid) bad |= code;
-                    if (c >= nvalid || code == 0xFFu) code = BITS == 4 ? 15u : 0u;  // padding / invalid
-                    out |= code << (BITS * (half * 8 + c));
+                    for (int c = 0; c < 8; ++c) {
+                        const uint32_t byte = ((c < 4 ? by.x : by.y) >> (8 * (c & 3))) & 0xFFu;
+                        uint32_t code = lut[byte];
+                        if (c < nvalid) bad |= code;
+                        if (c >= nvalid || code == 0xFFu) code = BITS == 4 ? 15u : 0u;  // padding / invalid
+                        out |= code << (BITS * (half * 8 + c));
+                    }
                 }
             }
-            words[sw0 + w] = out;
+            words[w0 + w] = out;
             if (bad & 0x80u) {
                 // first invalid byte of this word (rare path)
                 for (int c = 0; c < B; ++c) {
                     const int64_t p = int64_t(w) * B + c;
-                    if (p < slen && lut[ascii[sb0 + p]] == 0xFF) {
-                        atomicMin(status, (unsigned long long)(sb0 + p));
+                    if (p < len && lut[ascii[b0 + p]] == 0xFF) {
+                        atomicMin(status, (unsigned long long)(b0 + p));
                         break;
                     }
                 }
             }
+          }
         }
     }
 }
@@ -153,7 +156,7 @@ void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n,
     launch_status_init(status, s);
     if (n > 0) {
         const int64_t g8 = int64_t(sm_count_current()) * 8;
-        const int64_t need = (n + 255) / 256;  // 8 warps per block, 32 sequences per warp
+        const int64_t need = (n + 255) / 256;  // one thread per sequence
         const int grid = int(need < g8 ? need : g8);
         if (fmt == SALOBA_PACK4)
             pack_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
