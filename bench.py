@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--keep-order", type=int, default=0)
     ap.add_argument("--i16-rows", type=int, default=0)
     ap.add_argument("--grouped", action="store_true", help="config 5: components contiguous")
+    ap.add_argument("--dist-backend", default="nccl", help="test hook: gloo lets several ranks share one GPU")
     return ap.parse_args()
 
 
@@ -126,8 +127,8 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         if args.impl == "saloba":
-            torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if args.impl == "saloba" else "gloo")
+            torch.cuda.set_device(local % torch.cuda.device_count())
+        dist.init_process_group(args.dist_backend if args.impl == "saloba" else "gloo")
     elif args.impl == "saloba":
         torch.cuda.set_device(0)
     return world, rank, local
@@ -242,7 +243,10 @@ def main():
         o = sb.Options(args.force_group, args.force_path, args.keep_order, dp_ev, bins, args.i16_rows) if dp_ev else None
         s, qe, te = al.run(qa, qo, ta, to, h0, options=o)
         if world > 1:  # A5: results gathered to rank 0 (the only collective; none inside the DP)
-            dist.gather(al.out[:, :n], gather_buf if rank == 0 else None, dst=0)
+            if args.dist_backend == "nccl":
+                dist.gather(al.out[:, :n], gather_buf if rank == 0 else None, dst=0)
+            else:  # gloo test hook: host copies
+                dist.gather(al.out[:, :n].cpu(), [g.cpu() for g in gather_buf] if rank == 0 else None, dst=0)
         return s
 
     for _ in range(args.warmup):
@@ -277,6 +281,8 @@ def main():
     dp_ms = [a.elapsed_time(b) for a, b in dp_events]
     t = torch.tensor([ms, sum(dp_ms) / len(dp_ms)], dtype=torch.float64, device=dev)
     if world > 1:
+        if args.dist_backend != "nccl":
+            t = t.cpu()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, dp_ms_avg = float(t[0]), float(t[1])
     ms_per_step = ms_max / args.steps
@@ -301,6 +307,8 @@ def main():
         torch.cuda.synchronize()
         te2 = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
+            if args.dist_backend != "nccl":
+                te2 = te2.cpu()
             dist.all_reduce(te2, op=dist.ReduceOp.MAX)
         e2e_val = total_cells * args.e2e_steps / (float(te2[0]) * 1e-3) / 1e9
         h2d = int(len(batch.q_ascii) + len(batch.t_ascii) + 16 * (n + 1) + (4 * n if mode == sb.EXTEND else 0))
