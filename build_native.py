@@ -10,6 +10,7 @@ Products:
 """
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -52,22 +53,29 @@ def build_oracle(force: bool = False) -> str:
     return out
 
 
-def build_saloba(force: bool = False) -> str:
-    out = os.path.join(PKG, "libsaloba.so")
+def build_saloba(force: bool = False, out: str | None = None, defines: list[str] | None = None,
+                 objdir: str | None = None) -> str:
+    """libsaloba.so; `out`/`defines`/`objdir` build an experiment variant elsewhere (tools/variants.py)."""
+    out = out or os.path.join(PKG, "libsaloba.so")
+    objdir = objdir or os.path.join(ROOT, "build")
+    defines = defines or []
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     deps = srcs + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "saloba.h")]
     if not srcs:
         return out
     if force or _stale(out, deps):
-        objs = []
-        os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+        objs, jobs = [], []
+        os.makedirs(objdir, exist_ok=True)
         for s in srcs:
-            o = os.path.join(ROOT, "build", os.path.basename(s) + ".o")
+            o = os.path.join(objdir, os.path.basename(s) + ".o")
             if force or _stale(o, [s] + deps):
-                _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                      "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-warn-spills",
-                      "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o])
+                jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                             "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-warn-spills",
+                             *defines, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o])
             objs.append(o)
+        # translation units compile in parallel (dp_i16.cu dominates: ~100 kernel instances)
+        with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+            list(ex.map(_run, jobs))
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs])
     return out
 

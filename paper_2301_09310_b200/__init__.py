@@ -28,7 +28,8 @@ EXPORTS = ("saloba_packed_words", "saloba_pack", "saloba_workspace_bytes", "salo
            "saloba_strerror", "saloba_version", "saloba_kernel_launches")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libsaloba.so")
+# SALOBA_LIB: an alternative build of the same library (kernel A/B experiments, tools/variants.py)
+lib_path = os.environ.get("SALOBA_LIB") or os.path.join(_HERE, "libsaloba.so")
 _LIB = None
 
 

@@ -134,7 +134,11 @@ constexpr int STAGE_DEPTH = 3;
 template <int G>
 struct Stage {
     uint32_t q[STAGE_DEPTH][2][I16_THREADS];
+#ifdef SALOBA_NO_BSTAGE
     uint4 top[STAGE_DEPTH][I16_THREADS / G][4];
+#else
+    uint4 top[4][I16_THREADS / G][4];  // pass 1: slots 0..STAGE_DEPTH-1; pass 2: A rows 0..1, B rows 2..3
+#endif  // pass 1: slots 0..STAGE_DEPTH-1; pass 2: A rows 0..1, B rows 2..3
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -215,12 +219,23 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
     uint32_t botH[8], botF[8];
 #pragma unroll
     for (int x = 0; x < 8; ++x) botH[x] = botF[x] = 0;
+    uint32_t colbuf[PASS2 ? 8 : 1][R];  // pass 2: candidate columns of one step (local memory)
     const int steps = Q + G - 1;
+    // pass 2 stages the B-half checkpoint rows as well, at depth 2 (4 top-row slots per subwarp)
+#ifdef SALOBA_NO_BSTAGE
+    constexpr int DEPTH = STAGE_DEPTH;
+#else
+    constexpr int DEPTH = PASS2 ? 2 : STAGE_DEPTH;
+#endif
     // Inputs of step s+1 are fetched during step s with cp.async into a 2-slot shared-memory stage
     // (no registers held): every lane's 8 selectors, and on lane 0 the spilled top row(s) of its
     // next block.  Measured (ncu source view) before staging: the lane-0 top-row load was the top
     // stall of the kernel (~23% of samples), because the whole warp waits for it.
+#ifdef SALOBA_PROBE_NOSPILL  // perf probe only (wrong results): no spill traffic
+    const bool topA_mem = false;
+#else
     const bool topA_mem = io.topA != nullptr;
+#endif
     const bool topB_mem = PASS2 && io.topB != io.topA && io.topB != nullptr;
     auto prefetch = [&](int s2, int slot) {
         const int w2 = s2 - k;
@@ -233,26 +248,33 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
 #pragma unroll
                     for (int q = 0; q < 4; ++q) cp_async16(&st.top[slot][sub][q], io.topA + 16 * w2 + 4 * q);
                 }
-
+#ifndef SALOBA_NO_BSTAGE
+                if (topB_mem) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) cp_async16(&st.top[2 + slot][sub][q], io.topB + 16 * w2 + 4 * q);
+                }
+#endif
             }
         }
         cp_async_commit();
     };
 #pragma unroll
-    for (int p = 0; p < STAGE_DEPTH - 1; ++p) prefetch(p, p);
-    int cur = 0;  // stage slot of step s (s % STAGE_DEPTH)
+    for (int p = 0; p < DEPTH - 1; ++p) prefetch(p, p);
+    int cur = 0;  // stage slot of step s (s % DEPTH)
     // Every lane takes part in every step's shuffles (warp-uniform loop bounds, full mask); lanes
     // compute only while 0 <= w < Q.
     for (int s = 0; s < steps; ++s) {
         const int w = s - k;
         const bool active = unsigned(w) < unsigned(Q);
-        cp_async_wait<STAGE_DEPTH - 2>();  // this step's stage (issued STAGE_DEPTH-1 steps ago) has landed
-        prefetch(s + STAGE_DEPTH - 1, cur == 0 ? STAGE_DEPTH - 1 : cur - 1);
+        cp_async_wait<DEPTH - 2>();  // this step's stage (issued DEPTH-1 steps ago) has landed
+        prefetch(s + DEPTH - 1, cur == 0 ? DEPTH - 1 : cur - 1);
         uint32_t topH[8], topF[8], sel[8];
+        if constexpr (G > 1) {  // G == 1: the top row always comes from the spill row / boundary
 #pragma unroll
-        for (int x = 0; x < 8; ++x) {
-            topH[x] = __shfl_up_sync(mask, botH[x], 1, G);
-            topF[x] = __shfl_up_sync(mask, botF[x], 1, G);
+            for (int x = 0; x < 8; ++x) {
+                topH[x] = __shfl_up_sync(mask, botH[x], 1, G);
+                topF[x] = __shfl_up_sync(mask, botF[x], 1, G);
+            }
         }
         make_selectors(staged_codes<FMT>(st.q[cur][0][threadIdx.x], w, A.n),
                        staged_codes<FMT>(st.q[cur][1][threadIdx.x], w, B.n), sel);
@@ -274,10 +296,14 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
             }
             if (PASS2 && io.topB != io.topA) {  // high halves from half B's own checkpoint
                 uint32_t bh[8], bf[8];
-                if (topB_mem) {  // pass 2 only: not staged
+                if (topB_mem) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
+#ifdef SALOBA_NO_BSTAGE
                         const uint4 v = reinterpret_cast<const uint4*>(io.topB + 16 * w)[q];
+#else
+                        const uint4 v = st.top[2 + cur][sub][q];
+#endif
                         bh[2 * q] = v.x; bf[2 * q] = v.y; bh[2 * q + 1] = v.z; bf[2 * q + 1] = v.w;
                     }
                 } else {
@@ -296,9 +322,10 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
             }
         }
         const int cur_now = cur;
-        cur = (cur == STAGE_DEPTH - 1) ? 0 : cur + 1;
+        cur = (cur == DEPTH - 1) ? 0 : cur + 1;
         (void)cur_now;
         if (!active) continue;
+        unsigned cand = 0;  // pass 2: columns of this step that may hold `target`
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
             uint32_t hup = topH[x], fup = topF[x];
@@ -344,25 +371,60 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                 uint32_t cm = vmax3(vmax3(Hl[0], Hl[1], Hl[2]), vmax3(Hl[3], Hl[4], Hl[5]), vmax(Hl[6], Hl[7]));
 #pragma unroll
                 for (int r = 8; r < R; r += 2) cm = vmax3(cm, Hl[r], Hl[r + 1]);
-                const bool hitA = lo16(cm) >= lo16(target), hitB = hi16(cm) >= hi16(target);
-                if (hitA || hitB) {
-                    const int col = 8 * w + x;
+                // Where the pair maximum may sit in this column: LOCAL parks the column in local
+                // memory and scans it after the step, outside the unrolled hot code (ncu: 20%
+                // no-instruction stalls in pass 2 with a full scan inlined per column); EXTEND
+                // scans inline with a compact bit-mask (measured faster there: +2.3% vs parking).
+                constexpr bool HIT_INLINE = MODE == SALOBA_EXTEND;
+                if (HIT_INLINE && (lo16(cm) >= lo16(target) || hi16(cm) >= hi16(target))) {
+                    uint32_t mA = 0, mB = 0;
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        if (hitA && lo16(Hl[r]) == lo16(target) && (rA + r < hit[0] || (rA + r == hit[0] && col < hit[1]))) {
-                            hit[0] = rA + r;
-                            hit[1] = col;
-                        }
-                        if (hitB && hi16(Hl[r]) == hi16(target) && (rB + r < hit[2] || (rB + r == hit[2] && col < hit[3]))) {
-                            hit[2] = rB + r;
-                            hit[3] = col;
-                        }
+                        const uint32_t eq = __vcmpeq2(Hl[r], target);
+                        mA |= (eq & 1u) << r;
+                        mB |= (eq >> 31) << r;
+                    }
+                    const int col = 8 * w + x;
+                    if (mA) {
+                        const int r = rA + __ffs(mA) - 1;
+                        if (r < hit[0] || (r == hit[0] && col < hit[1])) { hit[0] = r; hit[1] = col; }
+                    }
+                    if (mB) {
+                        const int r = rB + __ffs(mB) - 1;
+                        if (r < hit[2] || (r == hit[2] && col < hit[3])) { hit[2] = r; hit[3] = col; }
+                    }
+                }
+                if (!HIT_INLINE && (lo16(cm) >= lo16(target) || hi16(cm) >= hi16(target))) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) colbuf[x][r] = Hl[r];
+                    cand |= 1u << x;
+                }
+            }
+        }
+        if (PASS2 && cand) {
+#pragma unroll 1
+            for (; cand; cand &= cand - 1) {
+                const int x = __ffs(cand) - 1, col = 8 * w + x;
+#pragma unroll 1
+                for (int r = 0; r < R; ++r) {
+                    const uint32_t h = colbuf[x][r];
+                    if (lo16(h) == lo16(target) && (rA + r < hit[0] || (rA + r == hit[0] && col < hit[1]))) {
+                        hit[0] = rA + r;
+                        hit[1] = col;
+                    }
+                    if (hi16(h) == hi16(target) && (rB + r < hit[2] || (rB + r == hit[2] && col < hit[3]))) {
+                        hit[2] = rB + r;
+                        hit[3] = col;
                     }
                 }
             }
         }
         corner = topH[7];
+#ifdef SALOBA_PROBE_NOSPILL
+        if (false) {
+#else
         if (io.bot && k == G - 1) {  // chunk-bottom row -> spill (interleaved H, F)
+#endif
             uint4* p = reinterpret_cast<uint4*>(io.bot + 16 * w);
 #pragma unroll
             for (int q = 0; q < 4; ++q) p[q] = make_uint4(botH[2 * q], botF[2 * q], botH[2 * q + 1], botF[2 * q + 1]);
