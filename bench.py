@@ -238,9 +238,11 @@ def main():
         gather_buf = [torch.empty((3, n), dtype=torch.int32, device=dev) for _ in range(world)] if rank == 0 else None
 
     bins = torch.zeros(16, dtype=torch.int32, device=dev)
+    long_group = torch.zeros(1, dtype=torch.int32, device=dev)
 
     def step(dp_ev=None):
-        o = sb.Options(args.force_group, args.force_path, args.keep_order, dp_ev, bins, args.i16_rows) if dp_ev else None
+        o = sb.Options(args.force_group, args.force_path, args.keep_order, dp_ev, bins, args.i16_rows,
+                       long_group) if dp_ev else None
         s, qe, te = al.run(qa, qo, ta, to, h0, options=o)
         if world > 1:  # A5: results gathered to rank 0 (the only collective; none inside the DP)
             if args.dist_backend == "nccl":
@@ -325,6 +327,7 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_mhz = csum["sm_mhz"] or 1965.0
     bc = bins.cpu().tolist()
+    lg = int(long_group.item())
     n16, n32 = sum(bc[8:15]), sum(bc[0:8])
     path = "int16x2" if n16 >= n32 else "int32"
     peak = sms * f_mhz * 1e6 * p_int / OPS_PER_CELL[path] / 1e9
@@ -340,7 +343,9 @@ def main():
             "frac": round(achieved / peak, 4), "traffic": traffic,
             "kernel": ("dp_i16_kernel" if path == "int16x2" else "dp_i32_kernel") +
                       " (all bins of one call, CUDA events on the launching stream)",
-            "bins": {f"{'i16' if b >= 8 else 'i32'}_G{1 << (b % 8)}": c for b, c in enumerate(bc) if c and b != 15},
+            # bin 13 = the int16x2 long bin, run at G = 2^long_group (16 or 32) this call
+            "bins": {f"{'i16' if b >= 8 else 'i32'}_G{1 << (lg if b == 13 else b % 8)}{'_long' if b == 13 else ''}": c
+                     for b, c in enumerate(bc) if c and b != 15},
             "dp_share_of_step": round(dp_ms_avg / ms_per_step, 3),
             "peak_derivation": f"{sms} SMs x {f_mhz:.0f} MHz (median under load) x {p_int:.0f} int lane-ops/clk/SM "
                                f"[{p_src}] / {OPS_PER_CELL[path]} ALU ops per cell ({path} path)"}

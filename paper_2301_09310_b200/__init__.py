@@ -48,7 +48,8 @@ class _Scoring(ctypes.Structure):
 class _Options(ctypes.Structure):
     _fields_ = [("force_group", ctypes.c_int32), ("force_path", ctypes.c_int32), ("keep_order", ctypes.c_int32),
                 ("i16_rows", ctypes.c_int32), ("ev_dp_begin", ctypes.c_void_p), ("ev_dp_end", ctypes.c_void_p),
-                ("bin_counts", ctypes.c_void_p), ("reserved", ctypes.c_int32 * 2)]
+                ("bin_counts", ctypes.c_void_p), ("long_group", ctypes.c_void_p),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 @dataclass(frozen=True)
@@ -76,6 +77,7 @@ class Options:
     dp_events: tuple | None = None  # (torch.cuda.Event, torch.cuda.Event) bracketing the DP kernels
     bin_counts: torch.Tensor | None = None  # cuda int32[16] <- pairs per bin (path*8 + log2 G)
     i16_rows: int = 0  # 0 default (16); 8 = 8 target rows per lane in the int16x2 kernel
+    long_group: torch.Tensor | None = None  # cuda int32[1] <- log2 G the long bin (13) ran with
 
     def _c(self) -> _Options:
         o = _Options(self.force_group, self.force_path, self.keep_order, self.i16_rows)
@@ -84,6 +86,8 @@ class Options:
             o.ev_dp_end = ctypes.c_void_p(self.dp_events[1].cuda_event)
         if self.bin_counts is not None:
             o.bin_counts = ctypes.c_void_p(self.bin_counts.data_ptr())
+        if self.long_group is not None:
+            o.long_group = ctypes.c_void_p(self.long_group.data_ptr())
         return o
 
 

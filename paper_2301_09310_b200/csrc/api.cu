@@ -15,7 +15,8 @@ namespace saloba {
 static std::atomic<long long> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-cudaError_t run_classify_sort(const ClassifyArgs& ca, const SortKV& kv, int32_t* bin_start, int sms, cudaStream_t s);
+cudaError_t run_classify_sort(const ClassifyArgs& ca, const SortKV& kv, int32_t* bin_start, int sms,
+                              int32_t* long_gidx, int64_t cap16, cudaStream_t s);
 size_t cub_sort_temp_bytes(int64_t n);
 void launch_status_init(int64_t* st, cudaStream_t s);
 void launch_status_final(int64_t* st, cudaStream_t s);
@@ -213,6 +214,8 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
     int32_t* bin_count = small;               // [NBINS]
     int32_t* bin_start = small + 32;          // [NBINS+1]
     int32_t* bin_counter = small + 64;        // [NBINS]
+    int32_t* long_qmax = small + 240;         // max Q of the long bin
+    int32_t* long_gidx = small + 241;         // group index chosen for the long bin
     if (cudaMemsetAsync(small, 0, 1024, s) != cudaSuccess) return SALOBA_ECUDA;
     launch_status_init(status, s);
 
@@ -221,8 +224,9 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
               ws + L.cub, L.cub_bytes};
     const int i16_rows = o.i16_rows == 8 ? 8 : I16_ROWS_DEFAULT;
     ClassifyArgs ca{q_words, q_word_off, int(fmt), sc.match, q_len, t_len, h0, n_pairs, int(mode), force_g, o.force_path, o.keep_order, i16_rows, Qsup * 8,
-                    score, q_end, t_end, kv.keys_in, kv.vals_in, bin_count, (unsigned long long*)status};
-    if (run_classify_sort(ca, kv, bin_start, d->sms, s) != cudaSuccess) return SALOBA_ECUDA;
+                    score, q_end, t_end, kv.keys_in, kv.vals_in, bin_count, (unsigned long long*)status, long_qmax};
+    const int64_t cap16 = int64_t(grid_for(d, int(mode), PATH_I16, NGROUPS - 2, i16_rows)) * (I16_THREADS / 16) * 2;
+    if (run_classify_sort(ca, kv, bin_start, d->sms, long_gidx, cap16, s) != cudaSuccess) return SALOBA_ECUDA;
 
     if (n_pairs > 0) {
         AlignArgs a{};
@@ -238,7 +242,9 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
         a.slot_bitmap = reinterpret_cast<uint32_t*>(small + 96);
         a.slot_words = (block_slots(d) + 31) / 32;
         a.i16_rows = i16_rows;
+        a.long_gidx = long_gidx;
         if (o.bin_counts) cudaMemcpyAsync(o.bin_counts, bin_count, NBINS * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+        if (o.long_group) cudaMemcpyAsync(o.long_group, long_gidx, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
         if (o.ev_dp_begin) cudaEventRecord((cudaEvent_t)o.ev_dp_begin, s);
         // All bins run as concurrent kernels (fork/join over the device's auxiliary streams), longest
         // bins first: a few long pairs then overlap the bulk of short ones instead of leaving most SMs
@@ -253,7 +259,13 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
             for (int g = NGROUPS - 1; g >= 0; --g, ++j) {
                 cudaStream_t as = aux[j % NAUX];
                 a.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(g), Qsup) + 8;
-                if (path == PATH_I16)
+                if (path == PATH_I16 && path * 8 + g == LONG_BIN) {
+                    // the long bin is launched at both widths; the one not chosen exits at once
+                    launch_dp_i16(int(mode), g, grid_for(d, int(mode), path, g, i16_rows), a, LONG_BIN, as);
+                    AlignArgs a16 = a;
+                    a16.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(g - 1), Qsup) + 8;
+                    launch_dp_i16(int(mode), g - 1, grid_for(d, int(mode), path, g - 1, i16_rows), a16, LONG_BIN, as);
+                } else if (path == PATH_I16)
                     launch_dp_i16(int(mode), g, grid_for(d, int(mode), path, g, i16_rows), a, path * 8 + g, as);
                 else
                     launch_dp_i32(int(mode), g, grid_for(d, int(mode), path, g), a, path * 8 + g, as);

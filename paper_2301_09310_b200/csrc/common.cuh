@@ -63,7 +63,13 @@ struct ClassifyArgs {
     uint32_t* vals;
     int32_t* bin_count;  // [NBINS]
     unsigned long long* status;
+    int32_t* long_qmax;  // max Q (8-base blocks) of the int16x2 long bin (atomicMax)
 };
+
+// Queries of >= LONG_Q blocks take the int16x2 "long bin" (bin PATH_I16*8 + NGROUPS-1); its width
+// (G=16 or G=32) is decided on the device once the bin is counted (long_bin_gidx).
+constexpr int LONG_Q = 256;
+constexpr int LONG_BIN = PATH_I16 * 8 + NGROUPS - 1;
 
 // Everything a DP kernel needs; passed by value.
 struct AlignArgs {
@@ -89,6 +95,7 @@ struct AlignArgs {
     uint32_t* slot_bitmap;    // one bit per block slot: set while a resident block owns it
     int32_t slot_words;       // 32-bit words in slot_bitmap
     int32_t i16_rows;         // target rows per lane of the int16x2 kernel (8 or 16)
+    const int32_t* long_gidx; // group index that runs LONG_BIN (set by bin_scan_kernel); others exit
 };
 
 // 8 consecutive bases [8w, 8w+8) of a packed sequence as 8 nibbles (base c in nibble c).

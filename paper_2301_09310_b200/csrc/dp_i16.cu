@@ -444,6 +444,8 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : I16_MINB16) dp_i16_k
     const int k = lane & (G - 1);
     const int64_t S = a.spill_stride;
     // per subwarp: 4 spill buffers (interleaved H,F rows of 2S words) inside this block's pool slot
+    constexpr int GIDX = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : G == 8 ? 3 : G == 16 ? 4 : 5;
+    if (bin == LONG_BIN && *a.long_gidx != GIDX) return;  // the long bin runs at the other width
     const int bslot = acquire_block_slot(a.slot_bitmap, a.slot_words);
     uint32_t* const spill = reinterpret_cast<uint32_t*>(a.spill) + bslot * a.block_slot_words + (threadIdx.x / G) * 8 * S;
     __shared__ Stage<G> st;

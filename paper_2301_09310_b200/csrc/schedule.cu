@@ -30,7 +30,7 @@ __host__ __device__ inline int choose_gidx(int Q, int m, int force_gidx, int min
     // long queries: every chunk-boundary row is Q*64 B, and with many resident subwarps the rows no
     // longer fit in L2.  Measured on config 4 (B200, round 1): G=16 6.1 TCUPS at 100k pairs, G=8
     // 3.8, G=4 3.4 -> long queries take G >= 16 (the cost model picks 16 or 32).
-    if (Q >= 256) min_gidx = 4;
+    if (Q >= LONG_Q) min_gidx = 4;
     int best = NGROUPS - 1;
     float bc = group_cost(Q, m, best, R, repass);
     for (int g = NGROUPS - 2; g >= min_gidx; --g) {
@@ -91,8 +91,12 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
         } else {
             const int Q = (n + 7) >> 3;
             const int path = (a.force_path != 1 && i16_eligible(a, k, n, m)) ? PATH_I16 : PATH_I32;
-            const int g = path == PATH_I16 ? choose_gidx(Q, m, a.force_gidx, 0, a.i16_rows, true)
-                                           : choose_gidx(Q, m, a.force_gidx, 0, I32_ROWS, false);
+            int g = path == PATH_I16 ? choose_gidx(Q, m, a.force_gidx, 0, a.i16_rows, true)
+                                     : choose_gidx(Q, m, a.force_gidx, 0, I32_ROWS, false);
+            if (path == PATH_I16 && a.force_gidx < 0 && g >= NGROUPS - 2) {
+                g = NGROUPS - 1;  // the long bin: G=16 or G=32 decided once it is counted
+                atomicMax(a.long_qmax, Q);
+            }
             bin = path * 8 + g;
             if (a.keep_order)
                 key = (uint64_t(bin) << 56) | uint64_t(k);
@@ -108,7 +112,13 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
     if (threadIdx.x < NBINS && cnt[threadIdx.x]) atomicAdd(a.bin_count + threadIdx.x, cnt[threadIdx.x]);
 }
 
-__global__ void bin_scan_kernel(const int32_t* count, int32_t* start) {
+// Long-bin width.  G=16 has the better throughput (config 4 alone, 88k long pairs: 5.49 vs 5.21
+// TCUPS) but twice the per-pair latency of G=32; when the bin holds only a few waves of pairs
+// (config 5: 8,950 long pairs among 10M short ones) those long items finish last and G=32 wins
+// (4.85 vs 4.16 TCUPS).  Rule: G=16 iff the bin fills >= 4 waves of G=16 subwarps and every query
+// fits G=16's spill stride.  cap16 = pairs one G=16 wave holds (2 per subwarp).
+__global__ void bin_scan_kernel(const int32_t* count, int32_t* start, const int32_t* long_qmax, int32_t* long_gidx,
+                                int64_t cap16, int force_gidx) {
     if (threadIdx.x == 0) {
         int acc = 0;
         for (int b = 0; b < NBINS; ++b) {
@@ -116,6 +126,8 @@ __global__ void bin_scan_kernel(const int32_t* count, int32_t* start) {
             acc += count[b];
         }
         start[NBINS] = acc;
+        const bool g16 = force_gidx < 0 && int64_t(count[LONG_BIN]) >= 4 * cap16 && *long_qmax <= qmax_for_gidx(NGROUPS - 2);
+        *long_gidx = g16 ? NGROUPS - 2 : NGROUPS - 1;
     }
 }
 
@@ -127,7 +139,7 @@ size_t cub_sort_temp_bytes(int64_t n) {
 }
 
 cudaError_t run_classify_sort(const ClassifyArgs& ca, const SortKV& kv, int32_t* bin_start, int sms,
-                              cudaStream_t s) {
+                              int32_t* long_gidx, int64_t cap16, cudaStream_t s) {
     if (ca.n > 0) {
         const int64_t g8 = int64_t(sms) * 8;
         const int grid = int((ca.n + 255) / 256 < g8 ? (ca.n + 255) / 256 : g8);
@@ -138,7 +150,7 @@ cudaError_t run_classify_sort(const ClassifyArgs& ca, const SortKV& kv, int32_t*
                                                         kv.vals_out, int(ca.n), 0, 64, s);
         if (e != cudaSuccess) return e;
     }
-    bin_scan_kernel<<<1, 32, 0, s>>>(ca.bin_count, bin_start);
+    bin_scan_kernel<<<1, 32, 0, s>>>(ca.bin_count, bin_start, ca.long_qmax, long_gidx, cap16, ca.force_gidx);
     count_launches(1);
     return cudaGetLastError();
 }

@@ -271,6 +271,26 @@ def test_config4_sampled(sb):
     _sample_check(sb, 4, n=2000, sample=40)
 
 
+@pytest.mark.parametrize("n_long", [2_000, 40_000])
+def test_long_bin_width_rule(sb, n_long):
+    """The int16x2 long bin (DESIGN.md §4 A2) runs at G=32 for a few waves of long pairs and at
+    G=16 once it holds >= 4 waves of G=16 subwarps; both widths are checked on sampled outputs."""
+    import torch
+
+    b = synth.generate(4, n_long, seed=11)
+    lg = torch.zeros(1, dtype=torch.int32, device="cuda")
+    bins = torch.zeros(16, dtype=torch.int32, device="cuda")
+    got = gpu_align(sb, b, sb.BWA_MEM, 0, sb.Options(bin_counts=bins, long_group=lg))
+    assert got[3] == -1
+    assert int(bins[13].item()) > 0
+    assert int(lg.item()) == (4 if n_long >= 40_000 else 5)
+    rng = np.random.default_rng(n_long)
+    idx = np.unique(np.concatenate([rng.choice(b.n, 24, replace=False),
+                                    np.argsort(b.qlen.astype(np.int64) * b.tlen)[-4:]]))
+    sub = b.subset(idx)
+    assert_same(tuple(x[idx] for x in got[:3]), oracle_align(sub, sb.BWA_MEM, 0), sub, f"long bin n={n_long}")
+
+
 def test_config5_sampled(sb):
     _sample_check(sb, 5, n=300_000, sample=3000)
 
