@@ -171,6 +171,31 @@ __device__ __forceinline__ uint32_t staged_codes(uint32_t word, int w, int len) 
     return x;
 }
 
+// Pass-2 hit search in one column of R rows (R <= 16): bit r of the low half / bit 16+r of the
+// high half of the result is set where row r equals the half's target (one VSETP-class compare and
+// one LOP3 per row for both halves).
+__device__ __forceinline__ uint32_t eq_bits(uint32_t h, uint32_t target, int r) {
+    return __vcmpeq2(h, target) & (0x00010001u << r);
+}
+// fold one column's hit bits into the first-hit-in-row-major-order record (rows first, then columns)
+__device__ __forceinline__ void take_hit(uint32_t bits, int col, int rA, int rB, int (&hit)[4]) {
+    const uint32_t mA = bits & 0xFFFFu, mB = bits >> 16;
+    if (mA) {
+        const int r = rA + __ffs(mA) - 1;
+        if (r < hit[0] || (r == hit[0] && col < hit[1])) {
+            hit[0] = r;
+            hit[1] = col;
+        }
+    }
+    if (mB) {
+        const int r = rB + __ffs(mB) - 1;
+        if (r < hit[2] || (r == hit[2] && col < hit[3])) {
+            hit[2] = r;
+            hit[3] = col;
+        }
+    }
+}
+
 template <int G, int R, int MODE, int FMT, bool PASS2>
 __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned mask, const int k, const int Q,
                                               const HalfInfo& A, const HalfInfo& B,
@@ -219,7 +244,9 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
     uint32_t botH[8], botF[8];
 #pragma unroll
     for (int x = 0; x < 8; ++x) botH[x] = botF[x] = 0;
-    uint32_t colbuf[PASS2 ? 8 : 1][R];  // pass 2: candidate columns of one step (local memory)
+    // pass 2: candidate columns of one step, parked in local memory (scalar words or quads, below)
+    uint32_t colbuf[PASS2 ? 8 : 1][R];
+    uint4 colbuf4[PASS2 ? 8 : 1][R / 4];
     const int steps = Q + G - 1;
     // pass 2 stages the B-half checkpoint rows as well, at depth 2 (4 top-row slots per subwarp)
 #ifdef SALOBA_NO_BSTAGE
@@ -371,32 +398,22 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                 uint32_t cm = vmax3(vmax3(Hl[0], Hl[1], Hl[2]), vmax3(Hl[3], Hl[4], Hl[5]), vmax(Hl[6], Hl[7]));
 #pragma unroll
                 for (int r = 8; r < R; r += 2) cm = vmax3(cm, Hl[r], Hl[r + 1]);
-                // Where the pair maximum may sit in this column: LOCAL parks the column in local
-                // memory and scans it after the step, outside the unrolled hot code (ncu: 20%
-                // no-instruction stalls in pass 2 with a full scan inlined per column); EXTEND
-                // scans inline with a compact bit-mask (measured faster there: +2.3% vs parking).
-                constexpr bool HIT_INLINE = MODE == SALOBA_EXTEND;
-                if (HIT_INLINE && (lo16(cm) >= lo16(target) || hi16(cm) >= hi16(target))) {
-                    uint32_t mA = 0, mB = 0;
+                // Where the pair maximum may sit in this column (rare per lane): park the column in
+                // local memory and scan it after the step, outside the unrolled hot code (ncu: 20%
+                // no-instruction stalls in pass 2 with a full scan inlined per column).  Measured
+                // on config 2 (B200): LOCAL is fastest with scalar words and a rolled scan (5.16 vs
+                // 4.98 TCUPS with quads), EXTEND with quads and an unrolled bit-mask scan (4.55 vs
+                // 4.41 scalar); neither order is explained by the SASS, so each mode keeps its best.
+                constexpr bool QUADS = MODE == SALOBA_EXTEND;
+                if (lo16(cm) >= lo16(target) || hi16(cm) >= hi16(target)) {
+                    if (QUADS) {
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const uint32_t eq = __vcmpeq2(Hl[r], target);
-                        mA |= (eq & 1u) << r;
-                        mB |= (eq >> 31) << r;
-                    }
-                    const int col = 8 * w + x;
-                    if (mA) {
-                        const int r = rA + __ffs(mA) - 1;
-                        if (r < hit[0] || (r == hit[0] && col < hit[1])) { hit[0] = r; hit[1] = col; }
-                    }
-                    if (mB) {
-                        const int r = rB + __ffs(mB) - 1;
-                        if (r < hit[2] || (r == hit[2] && col < hit[3])) { hit[2] = r; hit[3] = col; }
-                    }
-                }
-                if (!HIT_INLINE && (lo16(cm) >= lo16(target) || hi16(cm) >= hi16(target))) {
+                        for (int q = 0; q < R / 4; ++q)
+                            colbuf4[x][q] = make_uint4(Hl[4 * q], Hl[4 * q + 1], Hl[4 * q + 2], Hl[4 * q + 3]);
+                    } else {
 #pragma unroll
-                    for (int r = 0; r < R; ++r) colbuf[x][r] = Hl[r];
+                        for (int r = 0; r < R; ++r) colbuf[x][r] = Hl[r];
+                    }
                     cand |= 1u << x;
                 }
             }
@@ -405,16 +422,27 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
 #pragma unroll 1
             for (; cand; cand &= cand - 1) {
                 const int x = __ffs(cand) - 1, col = 8 * w + x;
-#pragma unroll 1
-                for (int r = 0; r < R; ++r) {
-                    const uint32_t h = colbuf[x][r];
-                    if (lo16(h) == lo16(target) && (rA + r < hit[0] || (rA + r == hit[0] && col < hit[1]))) {
-                        hit[0] = rA + r;
-                        hit[1] = col;
+                if (MODE == SALOBA_EXTEND) {
+                    uint32_t bits = 0;
+#pragma unroll
+                    for (int q = 0; q < R / 4; ++q) {
+                        const uint4 v = colbuf4[x][q];
+                        bits |= eq_bits(v.x, target, 4 * q) | eq_bits(v.y, target, 4 * q + 1) |
+                                eq_bits(v.z, target, 4 * q + 2) | eq_bits(v.w, target, 4 * q + 3);
                     }
-                    if (hi16(h) == hi16(target) && (rB + r < hit[2] || (rB + r == hit[2] && col < hit[3]))) {
-                        hit[2] = rB + r;
-                        hit[3] = col;
+                    take_hit(bits, col, rA, rB, hit);
+                } else {
+#pragma unroll 1
+                    for (int r = 0; r < R; ++r) {
+                        const uint32_t h = colbuf[x][r];
+                        if (lo16(h) == lo16(target) && (rA + r < hit[0] || (rA + r == hit[0] && col < hit[1]))) {
+                            hit[0] = rA + r;
+                            hit[1] = col;
+                        }
+                        if (hi16(h) == hi16(target) && (rB + r < hit[2] || (rB + r == hit[2] && col < hit[3]))) {
+                            hit[2] = rB + r;
+                            hit[3] = col;
+                        }
                     }
                 }
             }
