@@ -36,6 +36,8 @@ def _lib():
         lib.oracle_align_rows.argtypes = one
         lib.oracle_tables.argtypes = [p, i, p, i, i32, i32, i32, i32, i, i32, p, p, p, p]
         lib.oracle_align_batch.argtypes = [p, p, p, p, p, i64, i32, i32, i32, i32, i, p, p, p, p, i, i]
+        lib.oracle_start.argtypes = [p, i, p, i, i32, i32, i32, i32, p]
+        lib.oracle_start_batch.argtypes = [p, p, p, p, i64, i32, i32, i32, i32, p, p, p, p, p, p, i]
         _LIB = lib
     return _LIB
 
@@ -94,6 +96,33 @@ def align_batch(batch, match=1, mismatch=-4, alpha=7, beta=1, mode=LOCAL, thread
                                      score.ctypes.data, qe.ctypes.data, te.ctypes.data, st.ctypes.data,
                                      threads, int(rows))
     return score, qe, te, st, used
+
+
+def start(q, t, match=1, mismatch=-4, alpha=7, beta=1):
+    """(score, q_end, t_end, q_start, t_start) of one pair, LOCAL mode: the start by the reverse DP
+    over the prefixes ending at the end cell (oracle.c header; reading 15)."""
+    q, t = _b(q), _b(t)
+    out = (ctypes.c_int32 * 5)()
+    st = _lib().oracle_start(_buf(q), len(q), _buf(t), len(t), match, mismatch, alpha, beta, out)
+    if st != OK:
+        raise ValueError(st)
+    return tuple(int(x) for x in out)
+
+
+def start_batch(batch, match=1, mismatch=-4, alpha=7, beta=1, threads=None):
+    """LOCAL start coordinates over a synth.Batch-like object.
+
+    Returns (score, q_end, t_end, q_start, t_start, status, threads_used)."""
+    n = len(batch.q_off) - 1
+    outs = [np.empty(n, np.int32) for _ in range(6)]
+    threads = threads or os.cpu_count() or 1
+    qa = np.ascontiguousarray(batch.q_ascii)
+    ta = np.ascontiguousarray(batch.t_ascii)
+    qo = np.ascontiguousarray(batch.q_off, np.int64)
+    to = np.ascontiguousarray(batch.t_off, np.int64)
+    used = _lib().oracle_start_batch(qa.ctypes.data, qo.ctypes.data, ta.ctypes.data, to.ctypes.data, n,
+                                     match, mismatch, alpha, beta, *[o.ctypes.data for o in outs], threads)
+    return (*outs, used)
 
 
 def timed_sample(batch, seconds=10.0, mode=LOCAL, threads=None, **sc):

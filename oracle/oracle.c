@@ -28,6 +28,13 @@
  * S(t, q) = match if t == q and t != N, else mismatch (N never matches, N-N included: S:123-131).
  * Base codes (oracle's own table): A/a=0 C/c=1 G/g=2 T/t/U/u=3 N/n=4; others invalid.
  *
+ * START coordinates (LOCAL only, reading 15 — the paper defines no
+ * start): with (t_end, q_end) chosen by the tie rule above, align the reversed prefixes
+ * t' = t[t_end] t[t_end-1] .. t[0] and q' = q[q_end] .. q[0] in LOCAL mode; its end (i', j') by the
+ * same tie rule gives t_start = t_end - i', q_start = q_end - j' (the first aligned column of an
+ * optimal alignment ending at the end cell; among those, the largest t_start, then the largest
+ * q_start).  score 0: start = (0, 0), like the end.
+ *
  * Two entry points compute the same thing: oracle_align_full (the definition above, full
  * matrices, guarded at ORACLE_FULL_MAX_CELLS) and oracle_align_rows (the identical loop keeping
  * only rows i-1 and i; used for long pairs; cross-checked against the full one in tests).
@@ -232,6 +239,92 @@ EXPORT int oracle_align_rows(const uint8_t* q, int n, const uint8_t* t, int m, i
     free(qc);
     free(tc);
     return st;
+}
+
+/* ---- start coordinates by the reverse DP (LOCAL) ------------------------------------------ */
+/* out = {score, q_end, t_end, q_start, t_start}. */
+EXPORT int oracle_start(const uint8_t* q, int n, const uint8_t* t, int m, int32_t match, int32_t mismatch,
+                        int32_t alpha, int32_t beta, int32_t out[5]) {
+    int8_t *qc = NULL, *tc = NULL;
+    int st = prepare(q, n, t, m, OR_LOCAL, 0, &qc, &tc);
+    int32_t* rows = NULL;
+    int8_t *qr = NULL, *tr = NULL;
+    if (st == OR_OK) {
+        rows = (int32_t*)malloc(6 * (size_t)(n + 1) * sizeof(int32_t));
+        qr = (int8_t*)malloc((size_t)n);
+        tr = (int8_t*)malloc((size_t)m);
+        if (!rows || !qr || !tr) st = OR_ENOMEM;
+    }
+    if (st == OR_OK) {
+        int32_t fw[3], rv[3];
+        align_rows_impl(qc, n, tc, m, match, mismatch, alpha, beta, OR_LOCAL, 0, rows, fw);
+        out[0] = fw[0];
+        out[1] = fw[1];
+        out[2] = fw[2];
+        out[3] = 0;
+        out[4] = 0;
+        if (fw[0] > 0) {
+            const int qe = fw[1], te = fw[2];
+            for (int j = 0; j <= qe; ++j) qr[j] = qc[qe - j];
+            for (int i = 0; i <= te; ++i) tr[i] = tc[te - i];
+            align_rows_impl(qr, qe + 1, tr, te + 1, match, mismatch, alpha, beta, OR_LOCAL, 0, rows, rv);
+            out[3] = qe - rv[1];
+            out[4] = te - rv[2];
+        }
+    }
+    free(rows);
+    free(qr);
+    free(tr);
+    free(qc);
+    free(tc);
+    return st;
+}
+
+/* Batch form: q_start / t_start of every pair (LOCAL), pthreads over pairs. */
+typedef struct {
+    const uint8_t *q, *t;
+    const int64_t *q_off, *t_off;
+    int64_t n;
+    int32_t match, mismatch, alpha, beta;
+    int32_t *score, *q_end, *t_end, *q_start, *t_start, *status;
+    volatile int64_t next;
+} start_batch_t;
+
+static void* start_worker(void* arg) {
+    start_batch_t* b = (start_batch_t*)arg;
+    for (;;) {
+        int64_t k0 = __atomic_fetch_add(&b->next, 16, __ATOMIC_RELAXED);
+        if (k0 >= b->n) break;
+        int64_t k1 = k0 + 16 < b->n ? k0 + 16 : b->n;
+        for (int64_t k = k0; k < k1; ++k) {
+            int n = (int)(b->q_off[k + 1] - b->q_off[k]), m = (int)(b->t_off[k + 1] - b->t_off[k]);
+            int32_t out[5] = {-1, -2, -2, -2, -2};
+            int st = oracle_start(b->q + b->q_off[k], n, b->t + b->t_off[k], m, b->match, b->mismatch, b->alpha,
+                                  b->beta, out);
+            if (st) out[0] = -1, out[1] = out[2] = out[3] = out[4] = -2;
+            b->score[k] = out[0];
+            b->q_end[k] = out[1];
+            b->t_end[k] = out[2];
+            b->q_start[k] = out[3];
+            b->t_start[k] = out[4];
+            if (b->status) b->status[k] = st;
+        }
+    }
+    return NULL;
+}
+
+EXPORT int oracle_start_batch(const uint8_t* q, const int64_t* q_off, const uint8_t* t, const int64_t* t_off,
+                              int64_t n, int32_t match, int32_t mismatch, int32_t alpha, int32_t beta,
+                              int32_t* score, int32_t* q_end, int32_t* t_end, int32_t* q_start, int32_t* t_start,
+                              int32_t* status, int n_threads) {
+    start_batch_t b = {q, t, q_off, t_off, n, match, mismatch, alpha, beta,
+                       score, q_end, t_end, q_start, t_start, status, 0};
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > 512) n_threads = 512;
+    pthread_t th[512];
+    for (int k = 0; k < n_threads; ++k) pthread_create(&th[k], NULL, start_worker, &b);
+    for (int k = 0; k < n_threads; ++k) pthread_join(th[k], NULL);
+    return n_threads;
 }
 
 /* ---- batch driver: pthreads, dynamic pair scheduling ------------------------------------------ */

@@ -146,3 +146,75 @@ def kadane_gapfree(q: str, t: str, match=1, mismatch=-4):
             run = max(0, run + subst(t[i], q[j], match, mismatch))
             cells[(i, j)] = run
     return _pick(cells, 0, (0, 0))
+
+
+# ---- start coordinates (LOCAL, reading 15) ---------------------
+# The start of the reported alignment is the FIRST aligned column (t_start, q_start) of an optimal
+# alignment ending at the reported end cell; among several, the largest t_start, then the largest
+# q_start.  score 0: (0, 0).  Two routes, neither using a reversed DP:
+
+
+def brute_local_start(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1):
+    """(score, q_end, t_end, q_start, t_start) by explicit path enumeration (tiny inputs)."""
+    score, qe, te = brute_local(q, t, match, mismatch, alpha, beta)
+    if score == 0:
+        return 0, qe, te, 0, 0
+    n, m = len(q), len(t)
+    starts = []
+
+    def rec(i, j, total, last, s):
+        if (i, j) == (te, qe) and last == "M" and total == score:
+            starts.append(s)
+        if i + 1 < m and j + 1 < n:
+            rec(i + 1, j + 1, total + subst(t[i + 1], q[j + 1], match, mismatch), "M", s)
+        if j + 1 < n:
+            rec(i, j + 1, total - (beta if last == "I" else alpha), "I", s)
+        if i + 1 < m:
+            rec(i + 1, j, total - (beta if last == "D" else alpha), "D", s)
+
+    for i in range(te + 1):
+        for j in range(qe + 1):
+            rec(i, j, subst(t[i], q[j], match, mismatch), "M", (i, j))
+    ts, qs = max(starts)
+    return score, qe, te, qs, ts
+
+
+def anchored_global(q: str, t: str, qs, ts, qe, te, match=1, mismatch=-4, alpha=7, beta=1):
+    """Best value of an alignment of t[ts..te] with q[qs..qe] whose first and last columns are
+    aligned pairs (t_ts~q_qs, t_te~q_qe); cubic WSB form with an explicit gap cost, no E/F."""
+    a, b = t[ts:te + 1], q[qs:qe + 1]
+    m, n = len(a), len(b)
+    # V / I / D[i][j]: best value of a path from (0,0)[M] ending at (i,j) with last column an
+    # aligned pair / an insertion run / a deletion run (a run may follow a run of the other type)
+    V = [[NEG] * n for _ in range(m)]
+    I = [[NEG] * n for _ in range(m)]
+    D = [[NEG] * n for _ in range(m)]
+    V[0][0] = subst(a[0], b[0], match, mismatch)
+    for i in range(m):
+        for j in range(n):
+            if i > 0 and j > 0:
+                prev = max(V[i - 1][j - 1], I[i - 1][j - 1], D[i - 1][j - 1])
+                if prev > NEG:
+                    V[i][j] = prev + subst(a[i], b[j], match, mismatch)
+            for k in range(1, j + 1):
+                src = max(V[i][j - k], D[i][j - k])
+                if src > NEG:
+                    I[i][j] = max(I[i][j], src - _g(k, alpha, beta))
+            for k in range(1, i + 1):
+                src = max(V[i - k][j], I[i - k][j])
+                if src > NEG:
+                    D[i][j] = max(D[i][j], src - _g(k, alpha, beta))
+    return V[m - 1][n - 1]
+
+
+def anchored_local_start(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1):
+    """Same quantity by scanning candidate starts from the largest (t_start, q_start) down and
+    taking the first whose anchored alignment to the end cell reaches the score (WSB route)."""
+    score, qe, te = wsb_local(q, t, match, mismatch, alpha, beta)
+    if score == 0:
+        return 0, qe, te, 0, 0
+    for ts in range(te, -1, -1):
+        for qs in range(qe, -1, -1):
+            if anchored_global(q, t, qs, ts, qe, te, match, mismatch, alpha, beta) == score:
+                return score, qe, te, qs, ts
+    raise AssertionError("no start reaches the score")
