@@ -145,6 +145,39 @@ int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word_off, const
                        saloba_packing fmt, int32_t* score, int32_t* q_end, int32_t* t_end, void* workspace,
                        size_t workspace_bytes, int64_t* status, const saloba_options* opt, void* stream);
 
+/* ---- start coordinates (LOCAL mode) ----------------------------------- */
+
+/* The paper reports score and end only (SPEC S:16/S:215 put traceback out of scope).
+ * Start = the first aligned column (t_start, q_start) of an optimal alignment that ends at the
+ * reported end cell; among several, the largest t_start, then the largest q_start (DESIGN.md
+ * reading 15).  Computed without traceback by aligning the reversed prefixes t[t_end..0] and
+ * q[q_end..0] in LOCAL mode with the same kernels: start = end - (reversed end).
+ * (EXTEND alignments start at the seed anchor by definition, so they need no start pass.)
+ *
+ * Workspace for saloba_locate_start: n_pairs pairs whose packed query / target buffers hold
+ * q_words_total / t_words_total words (the reversed prefixes are written at the same word
+ * offsets) and whose queries are <= max_qlen bases.  0 on a bad argument or device. */
+size_t saloba_start_workspace_bytes(int64_t n_pairs, int64_t q_words_total, int64_t t_words_total,
+                                    int32_t max_qlen, int device);
+
+/* Start coordinates of LOCAL results produced by saloba_align_batch on the same packed pairs.
+ *   q_words, q_word_off, t_words, t_word_off, fmt   [dev] as passed to saloba_align_batch
+ *   q_words_total, t_words_total   capacity (words) of q_words / t_words
+ *   sc                              the scoring scheme of the forward call
+ *   score, q_end, t_end   [dev] int32[n_pairs]  the forward LOCAL results (input)
+ *   q_start, t_start      [dev] int32[n_pairs]  output: start coordinates (0-based, inclusive);
+ *                                               (0, 0) when score == 0; (-2, -2) when score < 0
+ *                                               (a pair the forward call rejected)
+ *   workspace             [dev] >= saloba_start_workspace_bytes(...), 256-byte aligned
+ *   status                [dev] int64[1]  -1, or the smallest pair index whose reversed pass did
+ *                                         not reproduce `score` (inconsistent input; start -3)
+ * Asynchronous on `stream`; host-checked errors as saloba_align_batch. */
+int saloba_locate_start(const uint32_t* q_words, const int64_t* q_word_off, int64_t q_words_total,
+                        const uint32_t* t_words, const int64_t* t_word_off, int64_t t_words_total, int64_t n_pairs,
+                        saloba_scoring sc, saloba_packing fmt, const int32_t* score, const int32_t* q_end,
+                        const int32_t* t_end, int32_t* q_start, int32_t* t_start, void* workspace,
+                        size_t workspace_bytes, int64_t* status, const saloba_options* opt, void* stream);
+
 /* ---- end-to-end from host buffers ----------------------------------------------------------- */
 
 /* Host-resident ASCII pairs in, host results out (the call a read mapper makes).  The batch is cut

@@ -15,7 +15,8 @@ import torch
 
 __all__ = [
     "LOCAL", "EXTEND", "PACK4", "PACK2", "Scoring", "Options", "BWA_MEM", "SalobaError", "lib", "lib_path",
-    "packed_words", "pack", "workspace_bytes", "align_batch", "align", "align_host", "version", "EXPORTS",
+    "packed_words", "pack", "workspace_bytes", "align_batch", "align", "start_workspace_bytes", "locate_start",
+    "align_host", "version", "EXPORTS",
 ]
 
 LOCAL, EXTEND = 0, 1
@@ -24,6 +25,7 @@ OK, EINVAL, ECUDA, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4
 
 #: every symbol include/saloba.h declares
 EXPORTS = ("saloba_packed_words", "saloba_pack", "saloba_workspace_bytes", "saloba_align_batch",
+           "saloba_start_workspace_bytes", "saloba_locate_start",
            "saloba_host_ctx_create", "saloba_host_ctx_destroy", "saloba_align_host_ctx", "saloba_align_host",
            "saloba_strerror", "saloba_version", "saloba_kernel_launches")
 
@@ -109,6 +111,11 @@ def lib() -> ctypes.CDLL:
         L.saloba_align_batch.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, _Scoring, ctypes.c_int, ctypes.c_int,
                                          vp, vp, vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(_Options), vp]
         L.saloba_align_batch.restype = ctypes.c_int
+        L.saloba_start_workspace_bytes.argtypes = [i64, i64, i64, i32, ctypes.c_int]
+        L.saloba_start_workspace_bytes.restype = ctypes.c_size_t
+        L.saloba_locate_start.argtypes = [vp, vp, i64, vp, vp, i64, i64, _Scoring, ctypes.c_int, vp, vp, vp, vp, vp,
+                                          vp, ctypes.c_size_t, vp, ctypes.POINTER(_Options), vp]
+        L.saloba_locate_start.restype = ctypes.c_int
         L.saloba_align_host.argtypes = [vp, vp, vp, vp, vp, i64, _Scoring, ctypes.c_int, vp, vp, vp, vp,
                                         ctypes.POINTER(_Options), vp]
         L.saloba_align_host.restype = ctypes.c_int
@@ -219,6 +226,45 @@ def align_batch(q_words, q_word_off, q_len, t_words, t_word_off, t_len, h0=None,
                                   _stream(stream))
     _check(rc, "saloba_align_batch")
     return score[:n], q_end[:n], t_end[:n], status
+
+
+def start_workspace_bytes(n_pairs: int, q_words_total: int, t_words_total: int, max_qlen: int,
+                          device: int | None = None) -> int:
+    dev = torch.cuda.current_device() if device is None else device
+    b = int(lib().saloba_start_workspace_bytes(n_pairs, q_words_total, t_words_total, max_qlen, dev))
+    if b == 0:
+        raise SalobaError(ECUDA, "saloba_start_workspace_bytes")
+    return b
+
+
+def locate_start(q_words, q_word_off, t_words, t_word_off, score, q_end, t_end, scoring: Scoring = BWA_MEM,
+                 fmt: int = PACK4, out=None, workspace: torch.Tensor | None = None, options: Options | None = None,
+                 max_qlen: int | None = None, stream=None):
+    """Start coordinates of LOCAL results (saloba_locate_start): returns (q_start, t_start, status).
+
+    q_words / t_words are the packed buffers the forward call used (their numel is the capacity);
+    score / q_end / t_end are its results."""
+    n = score.numel()
+    dev = score.device
+    if out is None:
+        out = torch.empty((2, max(n, 1)), dtype=torch.int32, device=dev)
+    q_start, t_start = out[0], out[1]
+    args = [_dev_tensor(a, d, nm) for a, d, nm in zip(
+        (q_words, q_word_off, t_words, t_word_off, score, q_end, t_end),
+        (torch.int32, torch.int64, torch.int32, torch.int64, torch.int32, torch.int32, torch.int32),
+        ("q_words", "q_word_off", "t_words", "t_word_off", "score", "q_end", "t_end"))]
+    qw, qwo, tw, two, sc_, qe, te = args
+    if workspace is None:
+        mq = int(qe.max().item()) + 1 if (max_qlen is None and n > 0) else (max_qlen or 1)
+        workspace = torch.empty(start_workspace_bytes(n, qw.numel(), tw.numel(), mq, dev.index), dtype=torch.uint8,
+                                device=dev)
+    status = torch.empty(1, dtype=torch.int64, device=dev)
+    opt = ctypes.byref(options._c()) if options is not None else None
+    rc = lib().saloba_locate_start(_p(qw), _p(qwo), qw.numel(), _p(tw), _p(two), tw.numel(), n, scoring._c(), fmt,
+                                   _p(sc_), _p(qe), _p(te), _p(q_start), _p(t_start), _p(workspace),
+                                   workspace.numel(), _p(status), opt, _stream(stream))
+    _check(rc, "saloba_locate_start")
+    return q_start[:n], t_start[:n], status
 
 
 def align(q_ascii, q_off, t_ascii, t_off, h0=None, scoring: Scoring = BWA_MEM, mode: int = LOCAL,

@@ -24,6 +24,11 @@ void launch_dp_i32(int mode, int gidx, int grid, const AlignArgs& a, int bin, cu
 const void* dp_i32_kernel_ptr(int mode, int gidx);
 void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s);
 const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt, int rows);
+void launch_reverse_prefix(int fmt, const uint32_t* words, const int64_t* word_off, const int32_t* end,
+                           const int32_t* score, int64_t n, uint32_t* out, int32_t* out_len, int sms, cudaStream_t s);
+void launch_start_finalize(const int32_t* score, const int32_t* q_end, const int32_t* t_end, const int32_t* rscore,
+                           const int32_t* rq_end, const int32_t* rt_end, int64_t n, int32_t* q_start,
+                           int32_t* t_start, int64_t* status, int sms, cudaStream_t s);
 void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n, int64_t base, int fmt,
                        uint32_t* words, int64_t* word_off, int32_t* lens, int64_t* status, cudaStream_t s);
 
@@ -291,6 +296,79 @@ SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word
                                   const saloba_options* opt, void* stream) {
     return align_batch_impl(q_words, q_word_off, q_len, t_words, t_word_off, t_len, h0, n_pairs, sc, mode, fmt, score,
                             q_end, t_end, workspace, workspace_bytes, status, opt, stream, nullptr);
+}
+
+// ---- start coordinates (LOCAL) -----------------------------------------
+namespace {
+struct StartLayout {
+    size_t rq, rt, rql, rtl, rres, inner, total;
+};
+StartLayout start_layout(int64_t n, int64_t qw, int64_t tw) {
+    StartLayout L{};
+    const size_t nn = size_t(std::max<int64_t>(n, 1));
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = off;
+        off = align_up(off + std::max<size_t>(bytes, 1), 256);
+        return at;
+    };
+    L.rq = take(size_t(std::max<int64_t>(qw, 1)) * 4);
+    L.rt = take(size_t(std::max<int64_t>(tw, 1)) * 4);
+    L.rql = take(nn * 4);
+    L.rtl = take(nn * 4);
+    L.rres = take(3 * nn * 4);
+    L.inner = off;
+    L.total = off;
+    return L;
+}
+}  // namespace
+
+SALOBA_API size_t saloba_start_workspace_bytes(int64_t n_pairs, int64_t q_words_total, int64_t t_words_total,
+                                               int32_t max_qlen, int device) {
+    if (n_pairs < 0 || q_words_total < 0 || t_words_total < 0) return 0;
+    const size_t inner = saloba_workspace_bytes(n_pairs, max_qlen, 0, device);
+    if (!inner) return 0;
+    return start_layout(n_pairs, q_words_total, t_words_total).total + inner;
+}
+
+SALOBA_API int saloba_locate_start(const uint32_t* q_words, const int64_t* q_word_off, int64_t q_words_total,
+                                   const uint32_t* t_words, const int64_t* t_word_off, int64_t t_words_total,
+                                   int64_t n_pairs, saloba_scoring sc, saloba_packing fmt, const int32_t* score,
+                                   const int32_t* q_end, const int32_t* t_end, int32_t* q_start, int32_t* t_start,
+                                   void* workspace, size_t workspace_bytes, int64_t* status,
+                                   const saloba_options* opt, void* stream) {
+    if (n_pairs < 0 || n_pairs > int64_t(INT32_MAX) - 1024 || !status || !workspace) return SALOBA_EINVAL;
+    if (n_pairs > 0 && (!q_words || !q_word_off || !t_words || !t_word_off || !score || !q_end || !t_end ||
+                        !q_start || !t_start || q_words_total < 1 || t_words_total < 1))
+        return SALOBA_EINVAL;
+    if (fmt != SALOBA_PACK4 && fmt != SALOBA_PACK2) return SALOBA_EINVAL;
+    if (!scheme_ok(sc)) return SALOBA_EINVAL;
+    if (reinterpret_cast<uintptr_t>(workspace) % 256) return SALOBA_EINVAL;
+    const StartLayout L = start_layout(n_pairs, q_words_total, t_words_total);
+    if (workspace_bytes <= L.total) return SALOBA_EWORKSPACE;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return SALOBA_ECUDA;
+    const DevInfo* d = dev_info(dev);
+    if (!d) return SALOBA_ECUDA;
+    char* ws = static_cast<char*>(workspace);
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t* rq = reinterpret_cast<uint32_t*>(ws + L.rq);
+    uint32_t* rt = reinterpret_cast<uint32_t*>(ws + L.rt);
+    int32_t* rql = reinterpret_cast<int32_t*>(ws + L.rql);
+    int32_t* rtl = reinterpret_cast<int32_t*>(ws + L.rtl);
+    int32_t* rres = reinterpret_cast<int32_t*>(ws + L.rres);
+    const int64_t nn = std::max<int64_t>(n_pairs, 1);
+    launch_reverse_prefix(int(fmt), q_words, q_word_off, q_end, score, n_pairs, rq, rql, d->sms, s);
+    launch_reverse_prefix(int(fmt), t_words, t_word_off, t_end, score, n_pairs, rt, rtl, d->sms, s);
+    // the reversed prefixes are aligned by the same schedule + DP kernels (LOCAL); `status`
+    // receives that call's status, then finalize adds any pair whose reversed score differs
+    const int rc = align_batch_impl(rq, q_word_off, rql, rt, t_word_off, rtl, nullptr, n_pairs, sc, SALOBA_LOCAL, fmt,
+                                    rres, rres + nn, rres + 2 * nn, ws + L.inner, workspace_bytes - L.inner, status,
+                                    opt, stream, nullptr);
+    if (rc != SALOBA_OK) return rc;
+    launch_start_finalize(score, q_end, t_end, rres, rres + nn, rres + 2 * nn, n_pairs, q_start, t_start, status,
+                          d->sms, s);
+    return cudaGetLastError() == cudaSuccess ? SALOBA_OK : SALOBA_ECUDA;
 }
 
 // ---- end-to-end from host buffers -----------------------------------------------------------
