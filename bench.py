@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--start-steps", type=int, default=3, help="LOCAL: time saloba_locate_start (0: skip)")
     ap.add_argument("--force-group", type=int, default=0)
     ap.add_argument("--force-path", type=int, default=0)
     ap.add_argument("--keep-order", type=int, default=0)
@@ -317,6 +318,33 @@ def main():
         e2e = {"value": round(e2e_val, 2), "unit": "GCUPS", "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": 12 * n * world, "api": "saloba_align_host_ctx (pinned host ASCII in, host results out, 8 pipelined slices)"}
 
+    # ---- NEXT-3: start coordinates of the same LOCAL results (saloba_locate_start), timed alone ----
+    start_pass = None
+    if mode == sb.LOCAL and args.start_steps > 0:
+        n_ = al.n
+        s_, qe_, te_ = al.out[0, :n_], al.out[1, :n_], al.out[2, :n_]
+        sws = torch.empty(sb.start_workspace_bytes(n_, al.q_words.numel(), al.t_words.numel(), max_q, dev.index),
+                          dtype=torch.uint8, device=dev)
+        sout = torch.empty((2, n_), dtype=torch.int32, device=dev)
+        args_s = (al.q_words, al.q_word_off[:-1], al.t_words, al.t_word_off[:-1], s_, qe_, te_, sb.BWA_MEM, sb.PACK4)
+        _, _, sst = sb.locate_start(*args_s, out=sout, workspace=sws)  # warm
+        torch.cuda.synchronize()
+        assert int(sst.item()) == -1
+        pc = int(((qe_.long() + 1) * (te_.long() + 1) * (s_ > 0).long()).sum().item())
+        l0 = sb.kernel_launches()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.start_steps):
+            sb.locate_start(*args_s, out=sout, workspace=sws)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        sms_ = s0.elapsed_time(s1) / args.start_steps
+        start_pass = {"ms_per_call": round(sms_, 3), "prefix_cells": pc,
+                      "gcups_prefix_cells": round(pc / (sms_ * 1e-3) / 1e9, 2),
+                      "forward_plus_start_gcups": round(cells_rank / ((ms_per_step + sms_) * 1e-3) / 1e9, 2),
+                      "launches_per_call": (sb.kernel_launches() - l0) // args.start_steps,
+                      "api": "saloba_locate_start (reversed prefixes through the same DP kernels)"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -362,6 +390,7 @@ def main():
                    "parallelism": f"pairs sharded over {world} GPU(s), results gathered to rank 0",
                    "gen_seconds": round(gen_s, 1)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "start_pass": start_pass,
         "clocks": {"sm_mhz": csum["sm_mhz"], "sm_max_mhz": csum["sm_max_mhz"], "reasons": csum["reasons"]},
     }
     print(json.dumps(line), flush=True)
