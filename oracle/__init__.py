@@ -36,6 +36,8 @@ def _lib():
         lib.oracle_align_rows.argtypes = one
         lib.oracle_tables.argtypes = [p, i, p, i, i32, i32, i32, i32, i, i32, p, p, p, p]
         lib.oracle_align_batch.argtypes = [p, p, p, p, p, i64, i32, i32, i32, i32, i, p, p, p, p, i, i]
+        lib.oracle_align_banded.argtypes = [p, i, p, i, i32, i32, i32, i32, i, i32, i32, p]
+        lib.oracle_banded_batch.argtypes = [p, p, p, p, p, p, i64, i32, i32, i32, i32, i, p, p, p, p, i]
         lib.oracle_start.argtypes = [p, i, p, i, i32, i32, i32, i32, p]
         lib.oracle_start_batch.argtypes = [p, p, p, p, i64, i32, i32, i32, i32, p, p, p, p, p, p, i]
         _LIB = lib
@@ -96,6 +98,33 @@ def align_batch(batch, match=1, mismatch=-4, alpha=7, beta=1, mode=LOCAL, thread
                                      score.ctypes.data, qe.ctypes.data, te.ctypes.data, st.ctypes.data,
                                      threads, int(rows))
     return score, qe, te, st, used
+
+
+def align_banded(q, t, w, match=1, mismatch=-4, alpha=7, beta=1, mode=LOCAL, h0=0):
+    """(score, q_end, t_end) with only the cells |i - j| <= w in the table (oracle.c header)."""
+    q, t = _b(q), _b(t)
+    out = (ctypes.c_int32 * 3)()
+    st = _lib().oracle_align_banded(_buf(q), len(q), _buf(t), len(t), match, mismatch, alpha, beta, mode, h0, w, out)
+    if st != OK:
+        raise ValueError(st)
+    return int(out[0]), int(out[1]), int(out[2])
+
+
+def banded_batch(batch, w, match=1, mismatch=-4, alpha=7, beta=1, mode=LOCAL, threads=None):
+    """Banded oracle over a synth.Batch-like object; w: int32[n] bands.  (score, q_end, t_end, status)."""
+    n = len(batch.q_off) - 1
+    outs = [np.empty(n, np.int32) for _ in range(4)]
+    threads = threads or os.cpu_count() or 1
+    qa = np.ascontiguousarray(batch.q_ascii)
+    ta = np.ascontiguousarray(batch.t_ascii)
+    qo = np.ascontiguousarray(batch.q_off, np.int64)
+    to = np.ascontiguousarray(batch.t_off, np.int64)
+    h0 = np.ascontiguousarray(batch.h0, np.int32)
+    ww = np.ascontiguousarray(w, np.int32)
+    _lib().oracle_banded_batch(qa.ctypes.data, qo.ctypes.data, ta.ctypes.data, to.ctypes.data, h0.ctypes.data,
+                               ww.ctypes.data, n, match, mismatch, alpha, beta, mode, *[o.ctypes.data for o in outs],
+                               threads)
+    return tuple(outs)
 
 
 def start(q, t, match=1, mismatch=-4, alpha=7, beta=1):

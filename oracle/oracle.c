@@ -28,6 +28,12 @@
  * S(t, q) = match if t == q and t != N, else mismatch (N never matches, N-N included: S:123-131).
  * Base codes (oracle's own table): A/a=0 C/c=1 G/g=2 T/t/U/u=3 N/n=4; others invalid.
  *
+ * BANDED (reading 16; PAPER.md P:1728-1735 names banded DP only as
+ * future work): a per-pair band w >= 0 keeps the cells with |i - j| <= w (the diagonal through the
+ * anchor / the table origin, as BWA-MEM's ksw_extend band).  Cells outside the band are not part
+ * of the table: they read as H = E = F = 0, exactly like the out-of-table boundary cells of
+ * LOCAL, and can never be the best cell.  Boundary row/column values (EXTEND) are unchanged.
+ *
  * START coordinates (LOCAL only, reading 15 — the paper defines no
  * start): with (t_end, q_end) chosen by the tie rule above, align the reversed prefixes
  * t' = t[t_end] t[t_end-1] .. t[0] and q' = q[q_end] .. q[0] in LOCAL mode; its end (i', j') by the
@@ -47,7 +53,7 @@
 #define EXPORT __attribute__((visibility("default")))
 
 enum { OR_LOCAL = 0, OR_EXTEND = 1 };
-enum { OR_OK = 0, OR_EINVALID_BASE = -1, OR_EEMPTY = -2, OR_ETOO_LARGE = -3, OR_EBAD_H0 = -4, OR_ENOMEM = -5 };
+enum { OR_OK = 0, OR_EINVALID_BASE = -1, OR_EEMPTY = -2, OR_ETOO_LARGE = -3, OR_EBAD_H0 = -4, OR_ENOMEM = -5, OR_EBAD_BAND = -6 };
 
 #define ORACLE_FULL_MAX_CELLS (1LL << 26)
 
@@ -133,6 +139,61 @@ static int align_full_impl(const int8_t* qc, int n, const int8_t* tc, int m, int
     out[0] = best;
     out[1] = bj; /* q_end */
     out[2] = bi; /* t_end */
+    return OR_OK;
+}
+
+/* ---- banded: the same definition with the cells |i - j| > w forced to zero ------------------ */
+static int align_banded_impl(const int8_t* qc, int n, const int8_t* tc, int m, int32_t match, int32_t mismatch,
+                             int32_t alpha, int32_t beta, int mode, int32_t h0, int32_t w, int32_t out[3]) {
+    const long W = n + 1;
+    int32_t* H = (int32_t*)malloc(3 * (size_t)(m + 1) * (size_t)W * sizeof(int32_t));
+    if (!H) return OR_ENOMEM;
+    int32_t* E = H + (size_t)(m + 1) * W;
+    int32_t* F = E + (size_t)(m + 1) * W;
+#define AT(X, i, j) X[((long)(i) + 1) * W + ((long)(j) + 1)]
+    for (int j = -1; j < n; ++j) {
+        AT(H, -1, j) = (mode == OR_EXTEND) ? ((j == -1) ? h0 : imax(0, h0 - alpha - beta * j)) : 0;
+        AT(E, -1, j) = 0;
+        AT(F, -1, j) = 0;
+    }
+    for (int i = 0; i < m; ++i) {
+        AT(H, i, -1) = (mode == OR_EXTEND) ? imax(0, h0 - alpha - beta * i) : 0;
+        AT(E, i, -1) = 0;
+        AT(F, i, -1) = 0;
+    }
+    for (int i = 0; i < m; ++i) {
+        for (int j = 0; j < n; ++j) {
+            if (i - j > w || j - i > w) { /* outside the band: not part of the table */
+                AT(E, i, j) = 0;
+                AT(F, i, j) = 0;
+                AT(H, i, j) = 0;
+                continue;
+            }
+            int32_t e = imax(0, imax(AT(H, i, j - 1) - alpha, AT(E, i, j - 1) - beta));
+            int32_t f = imax(0, imax(AT(H, i - 1, j) - alpha, AT(F, i - 1, j) - beta));
+            int32_t hd = AT(H, i - 1, j - 1);
+            int32_t d;
+            if (mode == OR_LOCAL || hd > 0) d = hd + subst(tc[i], qc[j], match, mismatch);
+            else d = 0;
+            AT(E, i, j) = e;
+            AT(F, i, j) = f;
+            AT(H, i, j) = imax(imax(0, e), imax(f, d));
+        }
+    }
+    int32_t best = (mode == OR_EXTEND) ? h0 : 0;
+    int32_t bi = (mode == OR_EXTEND) ? -1 : 0, bj = (mode == OR_EXTEND) ? -1 : 0;
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < n; ++j)
+            if (AT(H, i, j) > best) {
+                best = AT(H, i, j);
+                bi = i;
+                bj = j;
+            }
+#undef AT
+    free(H);
+    out[0] = best;
+    out[1] = bj;
+    out[2] = bi;
     return OR_OK;
 }
 
@@ -239,6 +300,65 @@ EXPORT int oracle_align_rows(const uint8_t* q, int n, const uint8_t* t, int m, i
     free(qc);
     free(tc);
     return st;
+}
+
+/* Banded alignment of one pair (w >= 0).  out = {score, q_end, t_end}. */
+EXPORT int oracle_align_banded(const uint8_t* q, int n, const uint8_t* t, int m, int32_t match, int32_t mismatch,
+                               int32_t alpha, int32_t beta, int mode, int32_t h0, int32_t w, int32_t out[3]) {
+    int8_t *qc = NULL, *tc = NULL;
+    int st = prepare(q, n, t, m, mode, h0, &qc, &tc);
+    if (st == OR_OK && w < 0) st = OR_EBAD_BAND;
+    if (st == OR_OK && (long long)(m + 1) * (n + 1) > ORACLE_FULL_MAX_CELLS) st = OR_ETOO_LARGE;
+    if (st == OR_OK) st = align_banded_impl(qc, n, tc, m, match, mismatch, alpha, beta, mode, h0, w, out);
+    free(qc);
+    free(tc);
+    return st;
+}
+
+typedef struct {
+    const uint8_t *q, *t;
+    const int64_t *q_off, *t_off;
+    const int32_t *h0, *w;
+    int64_t n;
+    int32_t match, mismatch, alpha, beta;
+    int mode;
+    int32_t *score, *q_end, *t_end, *status;
+    volatile int64_t next;
+} banded_batch_t;
+
+static void* banded_worker(void* arg) {
+    banded_batch_t* b = (banded_batch_t*)arg;
+    for (;;) {
+        int64_t k0 = __atomic_fetch_add(&b->next, 16, __ATOMIC_RELAXED);
+        if (k0 >= b->n) break;
+        int64_t k1 = k0 + 16 < b->n ? k0 + 16 : b->n;
+        for (int64_t k = k0; k < k1; ++k) {
+            int n = (int)(b->q_off[k + 1] - b->q_off[k]), m = (int)(b->t_off[k + 1] - b->t_off[k]);
+            int32_t out[3] = {-1, -2, -2};
+            int st = oracle_align_banded(b->q + b->q_off[k], n, b->t + b->t_off[k], m, b->match, b->mismatch,
+                                         b->alpha, b->beta, b->mode, b->h0 ? b->h0[k] : 0, b->w[k], out);
+            if (st) out[0] = -1, out[1] = -2, out[2] = -2;
+            b->score[k] = out[0];
+            b->q_end[k] = out[1];
+            b->t_end[k] = out[2];
+            if (b->status) b->status[k] = st;
+        }
+    }
+    return NULL;
+}
+
+EXPORT int oracle_banded_batch(const uint8_t* q, const int64_t* q_off, const uint8_t* t, const int64_t* t_off,
+                               const int32_t* h0, const int32_t* w, int64_t n, int32_t match, int32_t mismatch,
+                               int32_t alpha, int32_t beta, int mode, int32_t* score, int32_t* q_end,
+                               int32_t* t_end, int32_t* status, int n_threads) {
+    banded_batch_t b = {q, t, q_off, t_off, h0, w, n, match, mismatch, alpha, beta, mode,
+                        score, q_end, t_end, status, 0};
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > 512) n_threads = 512;
+    pthread_t th[512];
+    for (int k = 0; k < n_threads; ++k) pthread_create(&th[k], NULL, banded_worker, &b);
+    for (int k = 0; k < n_threads; ++k) pthread_join(th[k], NULL);
+    return n_threads;
 }
 
 /* ---- start coordinates by the reverse DP (LOCAL) ------------------------------------------ */

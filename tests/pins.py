@@ -37,12 +37,19 @@ def _pick(cells: dict, floor: int, floor_pos: tuple[int, int]):
     return best, bj, bi
 
 
-def brute_local(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1):
+def _inband(i, j, band):
+    return band is None or abs(i - j) <= band
+
+
+def brute_local(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1, band=None):
+    """band: None, or w >= 0 — paths may only visit cells with |i - j| <= w (NEXT-2)."""
     n, m = len(q), len(t)
     best: dict = {}
     sys.setrecursionlimit(10000)
 
     def rec(i, j, total, last):
+        if not _inband(i, j, band):
+            return
         key = (i, j)
         if total > best.get(key, NEG):
             best[key] = total
@@ -63,11 +70,13 @@ def brute_local(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1):
     return _pick(cells, 0, (0, 0))
 
 
-def brute_extend(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1, h0=10):
+def brute_extend(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1, h0=10, band=None):
     n, m = len(q), len(t)
     best: dict = {}
 
     def rec(i, j, total, last):
+        if i >= 0 and j >= 0 and not _inband(i, j, band):
+            return
         if i >= 0 and j >= 0 and total > best.get((i, j), NEG):
             best[(i, j)] = total
         if i + 1 < m and j + 1 < n:
@@ -91,11 +100,13 @@ def _g(k, alpha, beta):
     return alpha + (k - 1) * beta
 
 
-def wsb_local(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1):
+def wsb_local(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1, band=None):
     n, m = len(q), len(t)
     H = [[0] * (n + 1) for _ in range(m + 1)]  # H[i+1][j+1]
     for i in range(m):
         for j in range(n):
+            if not _inband(i, j, band):
+                continue  # outside the band: H stays 0
             v = max(0, H[i][j] + subst(t[i], q[j], match, mismatch))
             for k in range(1, j + 2):
                 v = max(v, H[i + 1][j + 1 - k] - _g(k, alpha, beta))
@@ -106,7 +117,7 @@ def wsb_local(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1):
     return _pick(cells, 0, (0, 0))
 
 
-def wsb_extend(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1, h0=10):
+def wsb_extend(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1, h0=10, band=None):
     n, m = len(q), len(t)
     H = [[0] * (n + 1) for _ in range(m + 1)]
     H[0][0] = h0
@@ -116,6 +127,8 @@ def wsb_extend(q: str, t: str, match=1, mismatch=-4, alpha=7, beta=1, h0=10):
         H[i + 1][0] = max(0, h0 - _g(i + 1, alpha, beta))
     for i in range(m):
         for j in range(n):
+            if not _inband(i, j, band):
+                continue
             hd = H[i][j]
             v = hd + subst(t[i], q[j], match, mismatch) if hd > 0 else 0
             v = max(0, v)
