@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--start-steps", type=int, default=3, help="LOCAL: time saloba_locate_start (0: skip)")
+    ap.add_argument("--band", type=int, default=-1, help="NEXT-2: also time saloba_align_banded with this w")
+    ap.add_argument("--band-steps", type=int, default=3)
     ap.add_argument("--force-group", type=int, default=0)
     ap.add_argument("--force-path", type=int, default=0)
     ap.add_argument("--keep-order", type=int, default=0)
@@ -345,6 +347,36 @@ def main():
                       "launches_per_call": (sb.kernel_launches() - l0) // args.start_steps,
                       "api": "saloba_locate_start (reversed prefixes through the same DP kernels)"}
 
+    # ---- NEXT-2: banded DP over the same packed batch (saloba_align_banded), timed alone ----
+    banded = None
+    if args.band >= 0:
+        n_ = al.n
+        wd = torch.full((n_,), args.band, dtype=torch.int32, device=dev)
+        bout = torch.empty((3, n_), dtype=torch.int32, device=dev)
+        bargs = (al.q_words, al.q_word_off[:-1], al.q_len[:n_], al.t_words, al.t_word_off[:-1], al.t_len[:n_], wd,
+                 h0 if mode == sb.EXTEND else None, sb.BWA_MEM, mode, sb.PACK4)
+        _, _, _, bst = sb.align_banded(*bargs, out=bout, workspace=al.ws)  # warm
+        torch.cuda.synchronize()
+        assert int(bst.item()) == -1
+        ql_, tl_ = batch.qlen.astype(np.int64), batch.tlen.astype(np.int64)
+        band_cells = 0
+        for d in range(-args.band, args.band + 1):  # cells on diagonal j - i = d inside the table
+            band_cells += int(np.maximum(0, np.minimum(tl_, ql_ - d) - max(0, -d)).sum())
+        l0 = sb.kernel_launches()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(args.band_steps):
+            sb.align_banded(*bargs, out=bout, workspace=al.ws)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bms = b0.elapsed_time(b1) / args.band_steps
+        banded = {"band_w": args.band, "ms_per_call": round(bms, 3), "band_cells": band_cells,
+                  "gcups_band_cells": round(band_cells / (bms * 1e-3) / 1e9, 2),
+                  "full_table_cells": cells_rank,
+                  "speedup_vs_unbanded_step": round(ms_per_step / bms, 3),
+                  "launches_per_call": (sb.kernel_launches() - l0) // args.band_steps,
+                  "api": "saloba_align_banded (exact int32 kernel, band-limited step ranges)"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -390,7 +422,7 @@ def main():
                    "parallelism": f"pairs sharded over {world} GPU(s), results gathered to rank 0",
                    "gen_seconds": round(gen_s, 1)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-        "start_pass": start_pass,
+        "start_pass": start_pass, "banded": banded,
         "clocks": {"sm_mhz": csum["sm_mhz"], "sm_max_mhz": csum["sm_max_mhz"], "reasons": csum["reasons"]},
     }
     print(json.dumps(line), flush=True)

@@ -145,6 +145,25 @@ int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word_off, const
                        saloba_packing fmt, int32_t* score, int32_t* q_end, int32_t* t_end, void* workspace,
                        size_t workspace_bytes, int64_t* status, const saloba_options* opt, void* stream);
 
+/* ---- banded DP ------------------------------------------------------------ */
+
+/* As saloba_align_batch, but pair k's table holds only the cells |i - j| <= band_w[k] (the band
+ * around the diagonal through the table origin / the EXTEND anchor, as BWA-MEM's extension band;
+ * PAPER.md P:1728-1735 names banded DP as the long-read direction).  Cells outside the band read
+ * as H = E = F = 0, like out-of-table cells, and are never computed: the work per pair is about
+ * t_len x (2 band_w + 8) cells instead of q_len x t_len (reading 16).
+ *   band_w  [dev] int32[n_pairs]  band half-width >= 0; a negative value is invalid data
+ *                                 (status / score -1, ends -2), band_w >= max(q_len, t_len) gives
+ *                                 the unbanded result.
+ * Banded pairs run on the exact int32 kernel; same workspace (saloba_workspace_bytes), same
+ * ownership, stream and error conventions as saloba_align_batch. */
+int saloba_align_banded(const uint32_t* q_words, const int64_t* q_word_off, const int32_t* q_len,
+                        const uint32_t* t_words, const int64_t* t_word_off, const int32_t* t_len,
+                        const int32_t* h0, const int32_t* band_w, int64_t n_pairs, saloba_scoring sc,
+                        saloba_mode mode, saloba_packing fmt, int32_t* score, int32_t* q_end, int32_t* t_end,
+                        void* workspace, size_t workspace_bytes, int64_t* status, const saloba_options* opt,
+                        void* stream);
+
 /* ---- start coordinates (LOCAL mode) ----------------------------------- */
 
 /* The paper reports score and end only (SPEC S:16/S:215 put traceback out of scope).

@@ -15,7 +15,7 @@ import torch
 
 __all__ = [
     "LOCAL", "EXTEND", "PACK4", "PACK2", "Scoring", "Options", "BWA_MEM", "SalobaError", "lib", "lib_path",
-    "packed_words", "pack", "workspace_bytes", "align_batch", "align", "start_workspace_bytes", "locate_start",
+    "packed_words", "pack", "workspace_bytes", "align_batch", "align", "align_banded", "start_workspace_bytes", "locate_start",
     "align_host", "version", "EXPORTS",
 ]
 
@@ -25,7 +25,7 @@ OK, EINVAL, ECUDA, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4
 
 #: every symbol include/saloba.h declares
 EXPORTS = ("saloba_packed_words", "saloba_pack", "saloba_workspace_bytes", "saloba_align_batch",
-           "saloba_start_workspace_bytes", "saloba_locate_start",
+           "saloba_align_banded", "saloba_start_workspace_bytes", "saloba_locate_start",
            "saloba_host_ctx_create", "saloba_host_ctx_destroy", "saloba_align_host_ctx", "saloba_align_host",
            "saloba_strerror", "saloba_version", "saloba_kernel_launches")
 
@@ -111,6 +111,9 @@ def lib() -> ctypes.CDLL:
         L.saloba_align_batch.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, _Scoring, ctypes.c_int, ctypes.c_int,
                                          vp, vp, vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(_Options), vp]
         L.saloba_align_batch.restype = ctypes.c_int
+        L.saloba_align_banded.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i64, _Scoring, ctypes.c_int, ctypes.c_int,
+                                          vp, vp, vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(_Options), vp]
+        L.saloba_align_banded.restype = ctypes.c_int
         L.saloba_start_workspace_bytes.argtypes = [i64, i64, i64, i32, ctypes.c_int]
         L.saloba_start_workspace_bytes.restype = ctypes.c_size_t
         L.saloba_locate_start.argtypes = [vp, vp, i64, vp, vp, i64, i64, _Scoring, ctypes.c_int, vp, vp, vp, vp, vp,
@@ -225,6 +228,38 @@ def align_batch(q_words, q_word_off, q_len, t_words, t_word_off, t_len, h0=None,
                                   _p(q_end), _p(t_end), _p(workspace), workspace.numel(), _p(status), opt,
                                   _stream(stream))
     _check(rc, "saloba_align_batch")
+    return score[:n], q_end[:n], t_end[:n], status
+
+
+def align_banded(q_words, q_word_off, q_len, t_words, t_word_off, t_len, band_w, h0=None,
+                 scoring: Scoring = BWA_MEM, mode: int = LOCAL, fmt: int = PACK4, out=None,
+                 workspace: torch.Tensor | None = None, options: Options | None = None, max_qlen: int | None = None,
+                 stream=None):
+    """Banded alignment (saloba_align_banded): only cells |i - j| <= band_w[k] are in pair k's table.
+    Returns (score, q_end, t_end, status) like align_batch."""
+    n = q_len.numel()
+    dev = q_len.device
+    if out is None:
+        out = torch.empty((3, max(n, 1)), dtype=torch.int32, device=dev)
+    score, q_end, t_end = out[0], out[1], out[2]
+    if workspace is None:
+        mq = int(q_len.max().item()) if (max_qlen is None and n > 0) else (max_qlen or 1)
+        workspace = torch.empty(workspace_bytes(n, mq, 0, dev.index), dtype=torch.uint8, device=dev)
+    status = torch.empty(1, dtype=torch.int64, device=dev)
+    opt = ctypes.byref(options._c()) if options is not None else None
+    if mode == EXTEND and h0 is None:
+        raise ValueError("EXTEND mode needs h0")
+    args = [q_words, q_word_off, q_len, t_words, t_word_off, t_len]
+    names = ["q_words", "q_word_off", "q_len", "t_words", "t_word_off", "t_len"]
+    dts = [torch.int32, torch.int64, torch.int32, torch.int32, torch.int64, torch.int32]
+    args = [_dev_tensor(a, d, nm) for a, d, nm in zip(args, dts, names)]
+    band_w = _dev_tensor(band_w, torch.int32, "band_w")
+    if h0 is not None:
+        h0 = _dev_tensor(h0, torch.int32, "h0")
+    rc = lib().saloba_align_banded(*[_p(a) for a in args], _p(h0), _p(band_w), n, scoring._c(), mode, fmt,
+                                   _p(score), _p(q_end), _p(t_end), _p(workspace), workspace.numel(), _p(status),
+                                   opt, _stream(stream))
+    _check(rc, "saloba_align_banded")
     return score[:n], q_end[:n], t_end[:n], status
 
 

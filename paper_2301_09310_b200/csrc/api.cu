@@ -21,7 +21,7 @@ size_t cub_sort_temp_bytes(int64_t n);
 void launch_status_init(int64_t* st, cudaStream_t s);
 void launch_status_final(int64_t* st, cudaStream_t s);
 void launch_dp_i32(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s);
-const void* dp_i32_kernel_ptr(int mode, int gidx);
+const void* dp_i32_kernel_ptr(int mode, int gidx, bool band);
 void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s);
 const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt, int rows);
 void launch_reverse_prefix(int fmt, const uint32_t* words, const int64_t* word_off, const int32_t* end,
@@ -58,9 +58,10 @@ static const DevInfo* dev_info(int device) {
         cudaSetDevice(device);
         for (int mode = 0; mode < 2; ++mode)
             for (int g = 0; g < NGROUPS; ++g) {
-                int nb = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i32_kernel_ptr(mode, g), BLOCK_THREADS, 0);
-                d.blocks_i32[mode][g] = std::max(1, nb);
+                int nb = 0, nbb = 0;  // plain and banded (NEXT-2) int32 kernels
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i32_kernel_ptr(mode, g, false), BLOCK_THREADS, 0);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, dp_i32_kernel_ptr(mode, g, true), BLOCK_THREADS, 0);
+                d.blocks_i32[mode][g] = std::max(1, std::max(nb, nbb));
                 for (int ri = 0; ri < 2; ++ri) {
                     nb = 0;
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i16_kernel_ptr(mode, g, SALOBA_PACK4, ri ? 16 : 8),
@@ -185,7 +186,7 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
                             const int32_t* h0, int64_t n_pairs, saloba_scoring sc, saloba_mode mode,
                             saloba_packing fmt, int32_t* score, int32_t* q_end, int32_t* t_end, void* workspace,
                             size_t workspace_bytes, int64_t* status, const saloba_options* opt, void* stream,
-                            const cudaStream_t* aux_in) {
+                            const cudaStream_t* aux_in, const int32_t* band_w = nullptr) {
     if (n_pairs < 0 || n_pairs > int64_t(INT32_MAX) - 1024) return SALOBA_EINVAL;
     if (!status || !workspace) return SALOBA_EINVAL;
     if (n_pairs > 0 && (!q_words || !q_word_off || !q_len || !t_words || !t_word_off || !t_len || !score ||
@@ -228,8 +229,9 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
               reinterpret_cast<uint32_t*>(ws + L.vals_in), reinterpret_cast<uint32_t*>(ws + L.vals_out),
               ws + L.cub, L.cub_bytes};
     const int i16_rows = o.i16_rows == 8 ? 8 : I16_ROWS_DEFAULT;
-    ClassifyArgs ca{q_words, q_word_off, int(fmt), sc.match, q_len, t_len, h0, n_pairs, int(mode), force_g, o.force_path, o.keep_order, i16_rows, Qsup * 8,
-                    score, q_end, t_end, kv.keys_in, kv.vals_in, bin_count, (unsigned long long*)status, long_qmax};
+    ClassifyArgs ca{q_words, q_word_off, int(fmt), sc.match, q_len, t_len, h0, n_pairs, int(mode), force_g,
+                    band_w ? 1 : o.force_path, o.keep_order, i16_rows, Qsup * 8, score, q_end, t_end, kv.keys_in,
+                    kv.vals_in, bin_count, (unsigned long long*)status, long_qmax, band_w};
     const int64_t cap16 = int64_t(grid_for(d, int(mode), PATH_I16, NGROUPS - 2, i16_rows)) * (I16_THREADS / 16) * 2;
     if (run_classify_sort(ca, kv, bin_start, d->sms, long_gidx, cap16, s) != cudaSuccess) return SALOBA_ECUDA;
 
@@ -248,6 +250,7 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
         a.slot_words = (block_slots(d) + 31) / 32;
         a.i16_rows = i16_rows;
         a.long_gidx = long_gidx;
+        a.band_w = band_w;
         if (o.bin_counts) cudaMemcpyAsync(o.bin_counts, bin_count, NBINS * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
         if (o.long_group) cudaMemcpyAsync(o.long_group, long_gidx, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
         if (o.ev_dp_begin) cudaEventRecord((cudaEvent_t)o.ev_dp_begin, s);
@@ -296,6 +299,19 @@ SALOBA_API int saloba_align_batch(const uint32_t* q_words, const int64_t* q_word
                                   const saloba_options* opt, void* stream) {
     return align_batch_impl(q_words, q_word_off, q_len, t_words, t_word_off, t_len, h0, n_pairs, sc, mode, fmt, score,
                             q_end, t_end, workspace, workspace_bytes, status, opt, stream, nullptr);
+}
+
+// ---- banded DP ----------------------------------------------------------
+SALOBA_API int saloba_align_banded(const uint32_t* q_words, const int64_t* q_word_off, const int32_t* q_len,
+                                   const uint32_t* t_words, const int64_t* t_word_off, const int32_t* t_len,
+                                   const int32_t* h0, const int32_t* band_w, int64_t n_pairs, saloba_scoring sc,
+                                   saloba_mode mode, saloba_packing fmt, int32_t* score, int32_t* q_end,
+                                   int32_t* t_end, void* workspace, size_t workspace_bytes, int64_t* status,
+                                   const saloba_options* opt, void* stream) {
+    if (n_pairs > 0 && !band_w) return SALOBA_EINVAL;
+    return align_batch_impl(q_words, q_word_off, q_len, t_words, t_word_off, t_len, h0, n_pairs, sc, mode, fmt, score,
+                            q_end, t_end, workspace, workspace_bytes, status, opt, stream, nullptr,
+                            n_pairs > 0 ? band_w : nullptr);
 }
 
 // ---- start coordinates (LOCAL) -----------------------------------------

@@ -64,6 +64,7 @@ struct ClassifyArgs {
     int32_t* bin_count;  // [NBINS]
     unsigned long long* status;
     int32_t* long_qmax;  // max Q (8-base blocks) of the int16x2 long bin (atomicMax)
+    const int32_t* band_w;  // NEXT-2: per-pair band half-width, or nullptr (banded pairs take the int32 path)
 };
 
 // Queries of >= LONG_Q blocks take the int16x2 "long bin" (bin PATH_I16*8 + NGROUPS-1); its width
@@ -96,6 +97,7 @@ struct AlignArgs {
     int32_t slot_words;       // 32-bit words in slot_bitmap
     int32_t i16_rows;         // target rows per lane of the int16x2 kernel (8 or 16)
     const int32_t* long_gidx; // group index that runs LONG_BIN (set by bin_scan_kernel); others exit
+    const int32_t* band_w;    // NEXT-2: per-pair band half-width (cells |i-j| <= w), or nullptr
 };
 
 // 8 consecutive bases [8w, 8w+8) of a packed sequence as 8 nibbles (base c in nibble c).

@@ -15,13 +15,21 @@
 // strict '>' across chunks keeps the earliest rows.
 // This path handles everything (N anywhere, both modes, the full int32 envelope of S:151) and is
 // the route for pairs the int16x2 path cannot take.
+//
+// BAND (reading 16): only cells |i - j| <= w are in the table, the
+// rest read as 0.  Lane k of chunk c (rows r0..r0+7) computes only blocks [blo, bhi] of columns
+// that meet the band; the chunk's step loop covers just the union of its lanes' ranges (so the
+// work is ~ rows x (2w + 8) instead of rows x n), plus one non-computing visit to block blo - 1
+// that delivers the top-left corner.  A lane that does not compute a block passes an all-zero
+// bottom row to the lane below (out-of-band cells are 0), lane 0 reads the previous chunk's spilled
+// row only where that chunk computed it, and blocks crossing the band edge mask their cells.
 #include <climits>
 
 #include "common.cuh"
 
 namespace saloba {
 
-template <int G, int MODE>
+template <int G, int MODE, bool BAND>
 __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int bin) {
     const int lane = threadIdx.x & 31;
     const int k = lane & (G - 1);
@@ -45,6 +53,7 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
         const uint32_t* __restrict__ qw = a.q_words + a.q_word_off[p];
         const uint32_t* __restrict__ tw = a.t_words + a.t_word_off[p];
         const int Q = (n + 7) >> 3, strips = (m + 7) >> 3, chunks = (strips + G - 1) / G;
+        const int wb = BAND ? a.band_w[p] : 0;  // band half-width (>= 0, validated by classify)
 
         int bestv = MODE ? h0 : 0, besti = MODE ? -1 : 0, bestj = MODE ? -1 : 0;
 
@@ -76,8 +85,24 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
 #pragma unroll
             for (int x = 0; x < 8; ++x) botH[x] = botF[x] = 0;
 
-            const int steps = Q + G - 1;
-            for (int s = 0; s < steps; ++s) {
+            // blocks of columns my rows meet inside the band (all of [0, Q) without a band), the
+            // previous chunk's last lane's upper block (its spilled row ends there), and the step
+            // range of the chunk: lane 0's first block - 1 (corner visit) .. lane G-1's last block
+            // Spill rows are indexed relative to the reading chunk's first block (roff for the row
+            // I read, woff for the row lane G-1 writes), so a banded row needs ~(2w + 8)/8 + 3
+            // blocks of capacity whatever the query length.
+            int blo = 0, bhi = Q - 1, bhi_prev = Q - 1, s_begin = 0, s_end = Q + G - 1, roff = 0, woff = 0;
+            if (BAND) {
+                blo = max(0, r0 - wb) >> 3;
+                bhi = min(Q - 1, (r0 + 7 + wb) >> 3);
+                bhi_prev = min(Q - 1, (c * G * 8 - 1 + wb) >> 3);
+                const int c0 = c * G * 8, c1 = min(m - 1, c0 + G * 8 - 1);
+                s_begin = max(0, (max(0, c0 - wb) >> 3) - 1);
+                s_end = min(Q - 1, (c1 + wb) >> 3) + G;  // exclusive
+                roff = s_begin;
+                woff = max(0, (max(0, c0 + G * 8 - wb) >> 3) - 1);  // s_begin of chunk c + 1
+            }
+            for (int s = s_begin; s < s_end; ++s) {
                 const int w = s - k;
                 int topH[8], topF[8];
 #pragma unroll
@@ -92,9 +117,12 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                             topH[x] = MODE ? max(0, h0 - al - be * (8 * w + x)) : 0;  // H(-1, j)
                             topF[x] = 0;
                         }
+                    } else if (BAND && w > bhi_prev) {  // never written by the previous chunk: out of band
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) topH[x] = topF[x] = 0;
                     } else {
-                        const int4* ph = reinterpret_cast<const int4*>(rdH + 8 * w);
-                        const int4* pf = reinterpret_cast<const int4*>(rdF + 8 * w);
+                        const int4* ph = reinterpret_cast<const int4*>(rdH + 8 * (w - roff));
+                        const int4* pf = reinterpret_cast<const int4*>(rdF + 8 * (w - roff));
                         int4 h0v = ph[0], h1v = ph[1], f0v = pf[0], f1v = pf[1];
                         topH[0] = h0v.x; topH[1] = h0v.y; topH[2] = h0v.z; topH[3] = h0v.w;
                         topH[4] = h1v.x; topH[5] = h1v.y; topH[6] = h1v.z; topH[7] = h1v.w;
@@ -102,8 +130,18 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                         topF[4] = f1v.x; topF[5] = f1v.y; topF[6] = f1v.z; topF[7] = f1v.w;
                     }
                 }
+                if (BAND && !(w >= blo && w <= bhi && r0 < m)) {
+                    // not computed: the corner of my next block (w >= 0: column -1's corner is the
+                    // boundary value set before the loop), and zeros for the lane below
+                    if (w >= 0) corner = topH[7];
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) botH[x] = botF[x] = 0;
+                    continue;
+                }
                 if (w >= 0 && w < Q && r0 < m) {
                     const uint32_t qword = load_block8(qw, w, a.fmt);
+                    // BAND: does this block cross the band edge? (then cells are masked)
+                    const bool edge = BAND && ((r0 + 7) - 8 * w > wb || (8 * w + 7) - r0 > wb);
                     int qc[8];
 #pragma unroll
                     for (int x = 0; x < 8; ++x) qc[x] = (8 * w + x < n) ? nib(qword, x) : 15;
@@ -118,24 +156,26 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                             const int f = max(hup - al, fup - be);
                             int d = hdiag + ((tc[r] == qc[x]) ? ma : mm);
                             if (MODE) d = (hdiag > 0) ? d : 0;
-                            const int h = max(max(0, e), max(f, d));
+                            int h = max(max(0, e), max(f, d));
+                            int ee = e, ff = f;
+                            if (BAND && edge && abs(r0 + r - col) > wb) h = ee = ff = 0;  // outside the band
                             if (h > bv[r]) {
                                 bv[r] = h;
                                 bc[r] = col;
                             }
                             hdiag = Hl[r];
                             Hl[r] = h;
-                            El[r] = e;
+                            El[r] = ee;
                             hup = h;
-                            fup = f;
+                            fup = ff;
                         }
                         botH[x] = hup;
                         botF[x] = fup;
                     }
                     corner = topH[7];
                     if (k == G - 1 && c + 1 < chunks) {
-                        int4* ph = reinterpret_cast<int4*>(wrH + 8 * w);
-                        int4* pf = reinterpret_cast<int4*>(wrF + 8 * w);
+                        int4* ph = reinterpret_cast<int4*>(wrH + 8 * (w - woff));
+                        int4* pf = reinterpret_cast<int4*>(wrF + 8 * (w - woff));
                         ph[0] = make_int4(botH[0], botH[1], botH[2], botH[3]);
                         ph[1] = make_int4(botH[4], botH[5], botH[6], botH[7]);
                         pf[0] = make_int4(botF[0], botF[1], botF[2], botF[3]);
@@ -181,37 +221,28 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
     release_block_slot(a.slot_bitmap, bslot);
 }
 
-template <int MODE>
-static void launch_i32_mode(int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s) {
+template <int MODE, bool BAND>
+static const void* kptr_mode(int gidx) {
     switch (gidx) {
-    case 0: dp_i32_kernel<1, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
-    case 1: dp_i32_kernel<2, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
-    case 2: dp_i32_kernel<4, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
-    case 3: dp_i32_kernel<8, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
-    case 4: dp_i32_kernel<16, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
-    default: dp_i32_kernel<32, MODE><<<grid, BLOCK_THREADS, 0, s>>>(a, bin); break;
+    case 0: return (const void*)dp_i32_kernel<1, MODE, BAND>;
+    case 1: return (const void*)dp_i32_kernel<2, MODE, BAND>;
+    case 2: return (const void*)dp_i32_kernel<4, MODE, BAND>;
+    case 3: return (const void*)dp_i32_kernel<8, MODE, BAND>;
+    case 4: return (const void*)dp_i32_kernel<16, MODE, BAND>;
+    default: return (const void*)dp_i32_kernel<32, MODE, BAND>;
     }
+}
+const void* dp_i32_kernel_ptr(int mode, int gidx, bool band) {
+    if (band) return mode == SALOBA_EXTEND ? kptr_mode<1, true>(gidx) : kptr_mode<0, true>(gidx);
+    return mode == SALOBA_EXTEND ? kptr_mode<1, false>(gidx) : kptr_mode<0, false>(gidx);
 }
 
 void launch_dp_i32(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s) {
-    if (mode == SALOBA_EXTEND) launch_i32_mode<1>(gidx, grid, a, bin, s);
-    else launch_i32_mode<0>(gidx, grid, a, bin, s);
+    const void* fn = dp_i32_kernel_ptr(mode, gidx, a.band_w != nullptr);
+    AlignArgs args = a;
+    void* params[] = {&args, &bin};
+    cudaLaunchKernel(fn, dim3(grid), dim3(BLOCK_THREADS), params, 0, s);
     count_launches(1);
-}
-
-template <int MODE>
-static const void* kptr_mode(int gidx) {
-    switch (gidx) {
-    case 0: return (const void*)dp_i32_kernel<1, MODE>;
-    case 1: return (const void*)dp_i32_kernel<2, MODE>;
-    case 2: return (const void*)dp_i32_kernel<4, MODE>;
-    case 3: return (const void*)dp_i32_kernel<8, MODE>;
-    case 4: return (const void*)dp_i32_kernel<16, MODE>;
-    default: return (const void*)dp_i32_kernel<32, MODE>;
-    }
-}
-const void* dp_i32_kernel_ptr(int mode, int gidx) {
-    return mode == SALOBA_EXTEND ? kptr_mode<1>(gidx) : kptr_mode<0>(gidx);
 }
 
 }  // namespace saloba

@@ -48,6 +48,30 @@ __host__ __device__ inline int choose_gidx(int Q, int m, int force_gidx, int min
 // int16x2 routing: bit-exact iff every H, E, F fits in int16 — all values lie in
 // [-alpha-2beta, B] with B = match*min(m,n) (LOCAL) or h0 + match*min(m,n) (EXTEND); EXTEND also
 // forms 2^k*H (2^k >= match+1) for its dead-zero rule.  Queries must be N-free (4-entry tables).
+// NEXT-2 banded pairs (int32 path): a chunk of G strips meets only the columns of its rows' band,
+// ~ (8G + 2w)/8 blocks, so the Q+G-1 ramp is paid on that width, not on Q.  Banded spill rows are
+// indexed relative to the chunk's first block (dp_i32.cu), so G only needs room for
+// min(Q, (2w + 8)/8 + 3) blocks.  G >= 2: the int32 kernel at G = 1 measured 3x slower than G = 2
+// on B200 (profiles/r01_ablation.json: 0.50 vs 1.49 TCUPS, config 2).
+__host__ __device__ inline int choose_gidx_banded(int Q, int m, int w, int force_gidx) {
+    const int need = min(Q, (2 * w + 8) / 8 + 3);
+    if (force_gidx >= 0 && need <= qmax_for_gidx(force_gidx)) return force_gidx;
+    int best = NGROUPS - 1;
+    float bc = 3.4e38f;
+    for (int g = NGROUPS - 1; g >= 1; --g) {
+        if (need > qmax_for_gidx(g)) continue;
+        const int G = 1 << g;
+        const int chunks = ((m + 7) / 8 + G - 1) / G;
+        const int width = min(Q, (8 * G + 2 * w + 7) / 8 + 1);
+        const float c = float(chunks) * float(width + G - 1) * float(G) + 0.1f * float(chunks - 1) * float(width);
+        if (c < bc) {
+            bc = c;
+            best = g;
+        }
+    }
+    return best;
+}
+
 __device__ inline bool i16_eligible(const ClassifyArgs& a, int64_t k, int n, int m) {
     const long long mn = n < m ? n : m;
     long long B = (long long)a.match * mn;
@@ -75,6 +99,7 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.n; k += int64_t(gridDim.x) * blockDim.x) {
         const int n = a.q_len[k], m = a.t_len[k];
         bool ok = n >= 1 && m >= 1 && n <= MAX_LEN && m <= MAX_LEN && n <= a.max_q_supported;
+        if (a.band_w) ok = ok && a.band_w[k] >= 0;
         if (a.mode == SALOBA_EXTEND) {
             const int h = a.h0[k];
             ok = ok && h >= 1 && h <= MAX_H0;
@@ -92,7 +117,8 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
             const int Q = (n + 7) >> 3;
             const int path = (a.force_path != 1 && i16_eligible(a, k, n, m)) ? PATH_I16 : PATH_I32;
             int g = path == PATH_I16 ? choose_gidx(Q, m, a.force_gidx, 0, a.i16_rows, true)
-                                     : choose_gidx(Q, m, a.force_gidx, 0, I32_ROWS, false);
+                    : a.band_w        ? choose_gidx_banded(Q, m, a.band_w[k], a.force_gidx)
+                                      : choose_gidx(Q, m, a.force_gidx, 0, I32_ROWS, false);
             if (path == PATH_I16 && a.force_gidx < 0 && g >= NGROUPS - 2) {
                 g = NGROUPS - 1;  // the long bin: G=16 or G=32 decided once it is counted
                 atomicMax(a.long_qmax, Q);
