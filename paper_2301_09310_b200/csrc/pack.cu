@@ -5,6 +5,8 @@
 // B = 8 (PACK4) or 16 (PACK2); ceil(len/B) <= floor(end/B) - floor(start/B) + 1 words fit.
 // A warp packs tiles of 8 consecutive sequences with lanes over the tile's flattened words, so
 // reads (8 bytes per lane) and 4-bit word writes coalesce and short sequences leave no lane idle.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace saloba {
@@ -133,6 +135,134 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ a
     }
 }
 
+// Flattened tile sweep (the default): a warp takes a tile of 32 consecutive sequences, scans their
+// word counts, and its lanes walk the tile's words in flattened order, so lane j of an iteration
+// packs the j-th word of the tile: consecutive lanes read consecutive 8-byte spans of the ASCII
+// and write consecutive words (both coalesced; the per-lane walk above issues 32 scattered sector
+// requests per load).  A 5-step shuffle binary search over the scan finds each word's sequence.
+template <int BITS>
+__global__ void __launch_bounds__(256) pack_tile_kernel(const uint8_t* __restrict__ ascii,
+                                                        const int64_t* __restrict__ byte_off, int64_t n_seqs,
+                                                        int64_t base, uint32_t* __restrict__ words,
+                                                        int64_t* __restrict__ word_off, int32_t* __restrict__ lens,
+                                                        unsigned long long* __restrict__ status) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int B = 32 / BITS;  // bases per word
+    __shared__ uint8_t lut[256];
+    build_lut(lut, BITS);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t total = byte_off[n_seqs];
+    const int64_t tiles = (n_seqs + 31) / 32;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
+    for (int64_t tile = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; tile < tiles; tile += warps) {
+        const int64_t s = tile * 32 + lane;
+        const bool has = s < n_seqs;
+        const int64_t b0 = has ? byte_off[s] : 0;
+        const int64_t len = has ? byte_off[s + 1] - b0 : 0;
+        const int64_t w0 = b0 / B + s + base;
+        if (has) {
+            word_off[s] = w0;
+            if (lens) lens[s] = int32_t(len);
+            if (s == n_seqs - 1) word_off[n_seqs] = byte_off[n_seqs] / B + n_seqs + base;
+        }
+        const int nw = int((len + B - 1) / B);
+        int incl = nw;  // inclusive scan of word counts over the tile
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const int tot = __shfl_sync(FULL, incl, 31);
+        constexpr int U = 4;  // words in flight per lane (memory-level parallelism)
+        for (int j0 = 0; j0 < tot; j0 += 32 * U) {
+          int wv[U];
+          int64_t ob0v[U], olenv[U], ow0v[U];
+          uint2 prev[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = j0 + 32 * u + lane;
+            // owner: the first lane whose inclusive count exceeds j
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+                const int v = __shfl_sync(FULL, incl, lo + step - 1);
+                if (v <= j) lo += step;
+            }
+            const int own = lo > 31 ? 31 : lo;
+            const int ex = __shfl_sync(FULL, incl - nw, own);
+            ob0v[u] = __shfl_sync(FULL, b0, own);
+            olenv[u] = __shfl_sync(FULL, len, own);
+            ow0v[u] = __shfl_sync(FULL, w0, own);
+            wv[u] = j < tot ? j - ex : -1;
+            prev[u] = wv[u] >= 0 ? load8(ascii, ob0v[u] + int64_t(wv[u]) * B, total) : make_uint2(0, 0);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (wv[u] < 0) continue;
+            const int w = wv[u];
+            const int64_t ob0 = ob0v[u], olen = olenv[u], ow0 = ow0v[u];
+            uint32_t out = 0, bad = 0;
+            bool fast = false;
+            const uint2 by0 = prev[u];
+            const int64_t rem = olen - int64_t(w) * B;  // bases left in the sequence from this word
+            if (BITS == 4 && rem < 8) {
+                // a sequence's last, partial word: bytes past the end read as 'A' for the fast check
+                // and become padding nibbles, so these words do not drag the warp onto the table path
+                const int nv = int(rem);
+                const uint32_t klo = nv >= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (8 * (4 - nv))) & (nv ? 0xFFFFFFFFu : 0u);
+                const uint32_t khi = nv >= 8 ? 0xFFFFFFFFu : nv <= 4 ? 0u : 0xFFFFFFFFu >> (8 * (8 - nv));
+                const uint2 by = make_uint2((by0.x & klo) | (0x41414141u & ~klo), (by0.y & khi) | (0x41414141u & ~khi));
+                uint32_t n0 = 0;
+                fast = fast_acgt8(by, n0);
+                out = n0 | (0xFFFFFFFFu << (4 * nv));
+            } else if (rem >= B) {
+                uint32_t n0 = 0;
+                fast = fast_acgt8(by0, n0);
+                if (BITS == 2 && fast) {
+                    uint32_t n1 = 0;
+                    fast = fast_acgt8(load8(ascii, ob0 + int64_t(w) * B + 8, total), n1);
+                    // 16 nibbles (each <= 3) -> 16 two-bit fields
+                    uint32_t a = n0, b = n1;
+                    a = (a | (a >> 2)) & 0x0F0F0F0Fu; a = (a | (a >> 4)) & 0x00FF00FFu; a = (a | (a >> 8)) & 0xFFFFu;
+                    b = (b | (b >> 2)) & 0x0F0F0F0Fu; b = (b | (b >> 4)) & 0x00FF00FFu; b = (b | (b >> 8)) & 0xFFFFu;
+                    out = a | (b << 16);
+                } else {
+                    out = n0;
+                }
+            }
+            if (!fast) {
+                out = 0;
+#pragma unroll
+                for (int half = 0; half < B / 8; ++half) {
+                    const int64_t p0 = int64_t(w) * B + half * 8;
+                    const uint2 by = half == 0 ? by0 : load8(ascii, ob0 + p0, total);
+                    const int nvalid = int(olen - p0 < 8 ? olen - p0 : 8);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint32_t byte = ((c < 4 ? by.x : by.y) >> (8 * (c & 3))) & 0xFFu;
+                        uint32_t code = lut[byte];
+                        if (c < nvalid) bad |= code;
+                        if (c >= nvalid || code == 0xFFu) code = BITS == 4 ? 15u : 0u;  // padding / invalid
+                        out |= code << (BITS * (half * 8 + c));
+                    }
+                }
+            }
+            words[ow0 + w] = out;
+            if (bad & 0x80u) {
+                for (int c = 0; c < B; ++c) {
+                    const int64_t p = int64_t(w) * B + c;
+                    if (p < olen && lut[ascii[ob0 + p]] == 0xFF) {
+                        atomicMin(status, (unsigned long long)(ob0 + p));
+                        break;
+                    }
+                }
+            }
+          }
+        }
+    }
+}
+
 __global__ void status_init(unsigned long long* st) { *st = ~0ull >> 1; }
 __global__ void status_final(unsigned long long* st) {
     if (*st == (~0ull >> 1)) *st = (unsigned long long)(-1ll);
@@ -156,14 +286,26 @@ void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n,
     launch_status_init(status, s);
     if (n > 0) {
         const int64_t g8 = int64_t(sm_count_current()) * 8;
-        const int64_t need = (n + 255) / 256;  // one thread per sequence
-        const int grid = int(need < g8 ? need : g8);
-        if (fmt == SALOBA_PACK4)
-            pack_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
-                                                (unsigned long long*)status);
-        else
-            pack_kernel<2><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
-                                                (unsigned long long*)status);
+        static const bool walk = getenv("SALOBA_PACK_WALK") != nullptr;  // A/B: the per-lane walk
+        if (walk) {
+            const int64_t need = (n + 255) / 256;  // one thread per sequence
+            const int grid = int(need < g8 ? need : g8);
+            if (fmt == SALOBA_PACK4)
+                pack_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
+                                                    (unsigned long long*)status);
+            else
+                pack_kernel<2><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
+                                                    (unsigned long long*)status);
+        } else {
+            const int64_t need = (n + 255) / 256;  // one warp per 32-sequence tile, 8 warps per block
+            const int grid = int(need < g8 ? need : g8);
+            if (fmt == SALOBA_PACK4)
+                pack_tile_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
+                                                         (unsigned long long*)status);
+            else
+                pack_tile_kernel<2><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
+                                                         (unsigned long long*)status);
+        }
         count_launches(1);
     }
     launch_status_final(status, s);
