@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--start-steps", type=int, default=3, help="LOCAL: time saloba_locate_start (0: skip)")
     ap.add_argument("--band", type=int, default=-1, help="NEXT-2: also time saloba_align_banded with this w")
     ap.add_argument("--band-steps", type=int, default=3)
+    ap.add_argument("--partition", default="balanced", choices=["balanced", "equal"],
+                    help="N>1: length-balanced (saloba_partition) or the paper's equal contiguous split")
     ap.add_argument("--force-group", type=int, default=0)
     ap.add_argument("--force-path", type=int, default=0)
     ap.add_argument("--keep-order", type=int, default=0)
@@ -224,7 +226,30 @@ def main():
         return t.numpy()[:nbytes]
 
     t0 = time.time()
-    batch = synth.generate(cfg, n, seed=cfg, first=rank * n, n_total=world * n, grouped=args.grouped, out=alloc)
+    n_total = world * n
+    partition_desc = "single GPU"
+    if world > 1 and args.partition == "balanced":
+        # A5: every rank computes the same length-balanced partition of the global
+        # batch on its own GPU (saloba_partition: cost sort + snake deal; deterministic, so no
+        # collective) and generates only the pairs it owns.
+        from paper_2301_09310_b200 import dist as sd
+
+        gql, gtl, _ = synth.shapes(cfg, n_total, seed=cfg, grouped=args.grouped)
+        owner = sd.balanced_partition(gql, gtl, world)
+        mine = np.nonzero(owner == rank)[0]
+        cost = sd.pair_cost(gql, gtl)
+        partition_desc = f"length-balanced snake over {world} ranks (saloba_partition), modelled max/mean {sd.imbalance(cost, owner, world):.4f}"
+        total_cells_global = int(np.dot(gql.astype(np.int64), gtl.astype(np.int64)))
+        counts = np.bincount(owner, minlength=world).tolist()
+        batch = synth.generate_idx(cfg, mine, n_total, seed=cfg, grouped=args.grouped, out=alloc)
+        del gql, gtl, owner, cost
+    else:
+        if world > 1:
+            partition_desc = f"equal contiguous split over {world} ranks"
+        batch = synth.generate(cfg, n, seed=cfg, first=rank * n, n_total=n_total, grouped=args.grouped, out=alloc)
+        counts = [n] * world
+        total_cells_global = None
+    n = batch.n  # pairs on this rank
     gen_s = time.time() - t0
     cells_rank = batch.cells()
     max_q = int(batch.qlen.max())
@@ -237,8 +262,10 @@ def main():
     al = sb.Aligner(n, int(batch.q_off[-1]), int(batch.t_off[-1]), max_q, sb.BWA_MEM, mode, sb.PACK4, opts)
     stream = torch.cuda.current_stream()
     gather_buf = None
+    nmax = max(counts)
+    send_buf = torch.full((3, nmax), -9, dtype=torch.int32, device=dev) if world > 1 else None
     if world > 1:
-        gather_buf = [torch.empty((3, n), dtype=torch.int32, device=dev) for _ in range(world)] if rank == 0 else None
+        gather_buf = [torch.empty((3, nmax), dtype=torch.int32, device=dev) for _ in range(world)] if rank == 0 else None
 
     bins = torch.zeros(16, dtype=torch.int32, device=dev)
     long_group = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -248,10 +275,11 @@ def main():
                        long_group) if dp_ev else None
         s, qe, te = al.run(qa, qo, ta, to, h0, options=o)
         if world > 1:  # A5: results gathered to rank 0 (the only collective; none inside the DP)
+            send_buf[:, :n].copy_(al.out[:, :n])  # ranks own different counts: padded to the max
             if args.dist_backend == "nccl":
-                dist.gather(al.out[:, :n], gather_buf if rank == 0 else None, dst=0)
+                dist.gather(send_buf, gather_buf if rank == 0 else None, dst=0)
             else:  # gloo test hook: host copies
-                dist.gather(al.out[:, :n].cpu(), [g.cpu() for g in gather_buf] if rank == 0 else None, dst=0)
+                dist.gather(send_buf.cpu(), [g.cpu() for g in gather_buf] if rank == 0 else None, dst=0)
         return s
 
     for _ in range(args.warmup):
@@ -291,7 +319,17 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, dp_ms_avg = float(t[0]), float(t[1])
     ms_per_step = ms_max / args.steps
-    total_cells = cells_rank * world
+    total_cells = total_cells_global if total_cells_global is not None else cells_rank * world
+    # per-rank balance of the measured step time (max/mean over ranks)
+    balance = None
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if args.dist_backend != "nccl":
+            tt = tt.cpu()
+        allt = [torch.zeros_like(tt) for _ in range(world)]
+        dist.all_gather(allt, tt)
+        per = [float(x[0]) for x in allt]
+        balance = round(max(per) / (sum(per) / len(per)), 4)
     value = total_cells * args.steps / (ms_max * 1e-3) / 1e9
 
     # ---- end-to-end through the host-buffer C-ABI entry point (H2D + pack + align + D2H) ----
@@ -318,7 +356,7 @@ def main():
         e2e_val = total_cells * args.e2e_steps / (float(te2[0]) * 1e-3) / 1e9
         h2d = int(len(batch.q_ascii) + len(batch.t_ascii) + 16 * (n + 1) + (4 * n if mode == sb.EXTEND else 0))
         e2e = {"value": round(e2e_val, 2), "unit": "GCUPS", "h2d_bytes_per_step": h2d * world,
-               "d2h_bytes_per_step": 12 * n * world, "api": "saloba_align_host_ctx (pinned host ASCII in, host results out, 8 pipelined slices)"}
+               "d2h_bytes_per_step": 12 * n * world, "api": "saloba_align_host_ctx (pinned host ASCII in, host results out, 4 pipelined slices of growing size)"}
 
     # ---- NEXT-3: start coordinates of the same LOCAL results (saloba_locate_start), timed alone ----
     start_pass = None
@@ -420,6 +458,7 @@ def main():
                    "cells_per_step": total_cells, "scoring": "match 1, mismatch -4, alpha 7, beta 1 (BWA-MEM-style)",
                    "l2": "inputs larger than L2 (ASCII %.0f MB per GPU per step)" % ((len(batch.q_ascii) + len(batch.t_ascii)) / 1e6),
                    "parallelism": f"pairs sharded over {world} GPU(s), results gathered to rank 0",
+                   "partition": partition_desc, "measured_rank_balance_max_over_mean": balance,
                    "gen_seconds": round(gen_s, 1)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "start_pass": start_pass, "banded": banded,

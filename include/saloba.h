@@ -197,6 +197,24 @@ int saloba_locate_start(const uint32_t* q_words, const int64_t* q_word_off, int6
                         const int32_t* t_end, int32_t* q_start, int32_t* t_start, void* workspace,
                         size_t workspace_bytes, int64_t* status, const saloba_options* opt, void* stream);
 
+/* ---- A5: length-balanced sharding over the GPUs of one box ------------------------ */
+
+/* Workspace (bytes) saloba_partition needs for n_pairs pairs (0 on a bad n_pairs). */
+size_t saloba_partition_workspace_bytes(int64_t n_pairs);
+
+/* Assign each pair to one of `world` ranks so that the modelled work is balanced (PAPER.md
+ * the paper's equal split leaves GPUs idle on skewed batches; it names "dynamic
+ * assignment or preprocessing with approximate sorting" as the fix).  cost = q_len*t_len + 2048,
+ * one stable radix sort by descending cost, then snake order over the ranks
+ * (0..W-1, W-1..0, ...).  Deterministic: every rank computing it from the same lengths gets the
+ * same assignment, so no collective is needed to agree on it.
+ *   q_len, t_len  [dev] int32[n_pairs]   lengths (negative values count as 0)
+ *   owner         [dev] int32[n_pairs]   output: rank of each pair, in 0..world-1
+ *   workspace     [dev] >= saloba_partition_workspace_bytes(n_pairs), 256-byte aligned
+ * Asynchronous on `stream`.  Host-checked errors only (EINVAL / EWORKSPACE). */
+int saloba_partition(const int32_t* q_len, const int32_t* t_len, int64_t n_pairs, int32_t world, int32_t* owner,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- end-to-end from host buffers ----------------------------------------------------------- */
 
 /* Host-resident ASCII pairs in, host results out (the call a read mapper makes).  The batch is cut

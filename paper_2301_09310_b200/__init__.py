@@ -15,7 +15,7 @@ import torch
 
 __all__ = [
     "LOCAL", "EXTEND", "PACK4", "PACK2", "Scoring", "Options", "BWA_MEM", "SalobaError", "lib", "lib_path",
-    "packed_words", "pack", "workspace_bytes", "align_batch", "align", "align_banded", "start_workspace_bytes", "locate_start",
+    "packed_words", "pack", "workspace_bytes", "align_batch", "align", "align_banded", "start_workspace_bytes", "locate_start", "partition",
     "align_host", "version", "EXPORTS",
 ]
 
@@ -26,6 +26,7 @@ OK, EINVAL, ECUDA, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4
 #: every symbol include/saloba.h declares
 EXPORTS = ("saloba_packed_words", "saloba_pack", "saloba_workspace_bytes", "saloba_align_batch",
            "saloba_align_banded", "saloba_start_workspace_bytes", "saloba_locate_start",
+           "saloba_partition_workspace_bytes", "saloba_partition",
            "saloba_host_ctx_create", "saloba_host_ctx_destroy", "saloba_align_host_ctx", "saloba_align_host",
            "saloba_strerror", "saloba_version", "saloba_kernel_launches")
 
@@ -114,6 +115,10 @@ def lib() -> ctypes.CDLL:
         L.saloba_align_banded.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i64, _Scoring, ctypes.c_int, ctypes.c_int,
                                           vp, vp, vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(_Options), vp]
         L.saloba_align_banded.restype = ctypes.c_int
+        L.saloba_partition_workspace_bytes.argtypes = [i64]
+        L.saloba_partition_workspace_bytes.restype = ctypes.c_size_t
+        L.saloba_partition.argtypes = [vp, vp, i64, i32, vp, vp, ctypes.c_size_t, vp]
+        L.saloba_partition.restype = ctypes.c_int
         L.saloba_start_workspace_bytes.argtypes = [i64, i64, i64, i32, ctypes.c_int]
         L.saloba_start_workspace_bytes.restype = ctypes.c_size_t
         L.saloba_locate_start.argtypes = [vp, vp, i64, vp, vp, i64, i64, _Scoring, ctypes.c_int, vp, vp, vp, vp, vp,
@@ -261,6 +266,18 @@ def align_banded(q_words, q_word_off, q_len, t_words, t_word_off, t_len, band_w,
                                    opt, _stream(stream))
     _check(rc, "saloba_align_banded")
     return score[:n], q_end[:n], t_end[:n], status
+
+
+def partition(q_len: torch.Tensor, t_len: torch.Tensor, world: int, stream=None) -> torch.Tensor:
+    """Length-balanced rank of each pair (saloba_partition): int32 cuda tensor in 0..world-1."""
+    q_len = _dev_tensor(q_len, torch.int32, "q_len")
+    t_len = _dev_tensor(t_len, torch.int32, "t_len")
+    n = q_len.numel()
+    owner = torch.empty(max(n, 1), dtype=torch.int32, device=q_len.device)
+    ws = torch.empty(int(lib().saloba_partition_workspace_bytes(n)), dtype=torch.uint8, device=q_len.device)
+    _check(lib().saloba_partition(_p(q_len), _p(t_len), n, world, _p(owner), _p(ws), ws.numel(), _stream(stream)),
+           "saloba_partition")
+    return owner[:n]
 
 
 def start_workspace_bytes(n_pairs: int, q_words_total: int, t_words_total: int, max_qlen: int,

@@ -395,7 +395,24 @@ __global__ void rebase_offsets(int64_t* off, int64_t n, int64_t base) {
 }
 }  // namespace saloba
 
-constexpr int HOST_SLICES = 8;
+constexpr int HOST_SLICES = 16;  // capacity; the slice count and shape are per context
+// Slice plan of the host path: SALOBA_HOST_SLICES slices (default 4, <= 16) whose sizes grow
+// linearly (1, 2, 3, 4: the first upload is short) unless SALOBA_HOST_RAMP=0.  Measured on B200
+// (config 2, tools/diag_e2e.py): 4 ramped slices 12.4-11.8 ms, 8 equal 13.0-13.3 ms, 16 equal 15.8 ms.
+static void host_slice_fracs(int& nsl, double* frac) {
+    const char* e = getenv("SALOBA_HOST_SLICES");
+    nsl = (e && *e) ? std::max(1, std::min(HOST_SLICES, atoi(e))) : 4;
+    const char* r = getenv("SALOBA_HOST_RAMP");
+    const bool ramp = !(r && *r == '0');
+    double tot = 0;
+    for (int i = 0; i < nsl; ++i) tot += ramp ? double(i + 1) : 1.0;
+    double acc = 0;
+    frac[0] = 0;
+    for (int i = 0; i < nsl; ++i) {
+        acc += ramp ? double(i + 1) : 1.0;
+        frac[i + 1] = acc / tot;
+    }
+}
 
 struct saloba_host_ctx {
     int device = 0;
@@ -456,7 +473,14 @@ SALOBA_API saloba_host_ctx* saloba_host_ctx_create(int64_t max_pairs, int64_t ma
     c->max_q_bytes = max_q_bytes;
     c->max_t_bytes = max_t_bytes;
     c->max_qlen = max_qlen;
-    c->slice_pairs = (max_pairs + HOST_SLICES - 1) / HOST_SLICES;
+    {
+        int nsl = 8;
+        double fr[HOST_SLICES + 1];
+        host_slice_fracs(nsl, fr);
+        double mx = 0;
+        for (int i = 0; i < nsl; ++i) mx = std::max(mx, fr[i + 1] - fr[i]);
+        c->slice_pairs = int64_t(double(max_pairs) * mx) + 2;
+    }
     c->qwcap = saloba_packed_words(max_q_bytes, max_pairs, SALOBA_PACK4);
     c->twcap = saloba_packed_words(max_t_bytes, max_pairs, SALOBA_PACK4);
     c->ws_bytes = saloba_workspace_bytes(std::max<int64_t>(c->slice_pairs, 1), max_qlen, 0, device);
@@ -521,9 +545,14 @@ SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii,
     cudaSetDevice(c->device);
     cudaStream_t s = (cudaStream_t)stream;
 
-    const int nsl = int(std::min<int64_t>(HOST_SLICES, n_pairs));
+    int nsl = 8;
+    double fr[HOST_SLICES + 1];
+    host_slice_fracs(nsl, fr);
+    nsl = int(std::min<int64_t>(nsl, n_pairs));
     int64_t cut[HOST_SLICES + 1];
-    for (int i = 0; i <= nsl; ++i) cut[i] = n_pairs * i / nsl;
+    for (int i = 0; i <= nsl; ++i) cut[i] = i == nsl ? n_pairs : std::min<int64_t>(n_pairs, int64_t(double(n_pairs) * fr[i]));
+    for (int i = 1; i <= nsl; ++i) cut[i] = std::max(cut[i], cut[i - 1] + 1);  // no empty slice
+    cut[nsl] = n_pairs;
     uint8_t* qd = static_cast<uint8_t*>(c->q);
     uint8_t* td = static_cast<uint8_t*>(c->t);
     int64_t* qo = static_cast<int64_t*>(c->qo);

@@ -19,21 +19,21 @@ def shard_range(n_total: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def pair_cost(qlen: np.ndarray, tlen: np.ndarray, kappa: float = 2048.0) -> np.ndarray:
-    """Modelled cost of a pair: cells + a per-pair overhead kappa."""
+    """Modelled cost of a pair, for REPORTING balance (the partition itself runs on the GPU with
+    the same model: saloba_partition): cells + a per-pair overhead kappa."""
     return qlen.astype(np.float64) * tlen.astype(np.float64) + kappa
 
 
-def balanced_partition(cost: np.ndarray, world: int) -> np.ndarray:
-    """Length-balanced assignment: sort by cost descending and deal in snake order
-    (0..W-1, W-1..0, ...).  Returns int32 rank per pair.  Max/mean rank cost -> 1 for large n."""
-    order = np.argsort(-cost, kind="stable")
-    n = len(cost)
-    k = np.arange(n)
-    rnd, pos = k // world, k % world
-    snake = np.where(rnd % 2 == 0, pos, world - 1 - pos)
-    owner = np.empty(n, np.int32)
-    owner[order] = snake.astype(np.int32)
-    return owner
+def balanced_partition(qlen, tlen, world: int) -> np.ndarray:
+    """Length-balanced rank per pair, computed on the current GPU by saloba_partition (cost sort +
+    snake deal, include/saloba.h).  Deterministic, so every rank can compute it from the global
+    lengths without a collective.  qlen / tlen: numpy or torch int32.  Returns int32 numpy."""
+    from . import partition
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    q = torch.as_tensor(np.asarray(qlen, np.int32)).to(dev)
+    t = torch.as_tensor(np.asarray(tlen, np.int32)).to(dev)
+    return partition(q, t, world).cpu().numpy()
 
 
 def imbalance(cost: np.ndarray, owner: np.ndarray, world: int) -> float:

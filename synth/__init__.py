@@ -34,6 +34,10 @@ def _lib():
                                       i32p, i32p, i32p, ctypes.c_int]
         lib.synth_bases.argtypes = [ctypes.c_int, ctypes.c_uint64, i64, i64, i64, ctypes.c_int,
                                     ctypes.c_double, i64p, i64p, u8p, u8p, ctypes.c_int]
+        lib.synth_lengths_idx.argtypes = [ctypes.c_int, ctypes.c_uint64, i64p, i64, i64, ctypes.c_int,
+                                          i32p, i32p, i32p, ctypes.c_int]
+        lib.synth_bases_idx.argtypes = [ctypes.c_int, ctypes.c_uint64, i64p, i64, i64, ctypes.c_int,
+                                        ctypes.c_double, i64p, i64p, u8p, u8p, ctypes.c_int]
         _LIB = lib
     return _LIB
 
@@ -115,6 +119,24 @@ def generate(cfg: int, n: int | None = None, seed: int | None = None, first: int
         ta = out("t", int(to[-1]))
     _lib().synth_bases(cfg, seed, first, n, n_total, int(grouped), float(p_n), _ptr(qo), _ptr(to),
                        _ptr(qa), _ptr(ta), threads or os.cpu_count() or 1)
+    return Batch(qa, qo, ta, to, h0)
+
+
+def generate_idx(cfg: int, idx: np.ndarray, n_total: int, seed: int | None = None, grouped: bool = False,
+                 p_n: float = 0.0, threads: int | None = None, out=None) -> Batch:
+    """Pairs idx[0], idx[1], ... of the n_total-pair batch of config `cfg` (a rank's shard of a
+    partitioned batch); identical to the same pairs of generate(cfg, n_total)."""
+    idx = np.ascontiguousarray(idx, np.int64)
+    n = len(idx)
+    seed = cfg if seed is None else seed
+    th = threads or os.cpu_count() or 1
+    ql, tl, h0 = (np.empty(n, np.int32) for _ in range(3))
+    _lib().synth_lengths_idx(cfg, seed, _ptr(idx), n, n_total, int(grouped), _ptr(ql), _ptr(tl), _ptr(h0), th)
+    qo, to = offsets(ql), offsets(tl)
+    qa = out("q", int(qo[-1])) if out else np.empty(int(qo[-1]), np.uint8)
+    ta = out("t", int(to[-1])) if out else np.empty(int(to[-1]), np.uint8)
+    _lib().synth_bases_idx(cfg, seed, _ptr(idx), n, n_total, int(grouped), float(p_n), _ptr(qo), _ptr(to),
+                           _ptr(qa), _ptr(ta), th)
     return Batch(qa, qo, ta, to, h0)
 
 

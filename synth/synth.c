@@ -218,13 +218,16 @@ typedef struct {
     int32_t *qlen, *tlen, *h0;
     const int64_t *q_off, *t_off;
     uint8_t *q, *t;
+    const int64_t* idx; /* optional: global pair index of output i (else first + i) */
 } job_t;
+
+static inline int64_t pair_index(const job_t* j, int64_t i) { return j->idx ? j->idx[i] : j->first + i; }
 
 static void* len_worker(void* arg) {
     job_t* j = (job_t*)arg;
     for (int64_t i = j->lo; i < j->hi; ++i) {
         pair_shape_t sh;
-        simulate_pair(j->cfg, j->seed, j->first + i, j->n_total, j->grouped, j->p_n, &sh, NULL, NULL);
+        simulate_pair(j->cfg, j->seed, pair_index(j, i), j->n_total, j->grouped, j->p_n, &sh, NULL, NULL);
         j->qlen[i] = sh.qlen;
         j->tlen[i] = sh.tlen;
         if (j->h0) j->h0[i] = sh.h0;
@@ -235,7 +238,7 @@ static void* base_worker(void* arg) {
     job_t* j = (job_t*)arg;
     for (int64_t i = j->lo; i < j->hi; ++i) {
         pair_shape_t sh;
-        simulate_pair(j->cfg, j->seed, j->first + i, j->n_total, j->grouped, j->p_n, &sh,
+        simulate_pair(j->cfg, j->seed, pair_index(j, i), j->n_total, j->grouped, j->p_n, &sh,
                       j->q + j->q_off[i], j->t + j->t_off[i]);
     }
     return NULL;
@@ -259,8 +262,24 @@ static void run_jobs(job_t proto, int n_threads, void* (*fn)(void*)) {
  * grouped config-5 order).  h0 may be NULL. Returns 0. */
 EXPORT int synth_lengths(int cfg, uint64_t seed, int64_t first, int64_t n, int64_t n_total, int grouped,
                          int32_t* qlen, int32_t* tlen, int32_t* h0, int n_threads) {
-    job_t j = {cfg, grouped, seed, first, n, n_total, 0, 0, 0.0, qlen, tlen, h0, NULL, NULL, NULL, NULL};
+    job_t j = {cfg, grouped, seed, first, n, n_total, 0, 0, 0.0, qlen, tlen, h0, NULL, NULL, NULL, NULL, NULL};
     run_jobs(j, n_threads, len_worker);
+    return 0;
+}
+
+/* As synth_lengths / synth_bases for an explicit list of global pair indices idx[0..n) (a rank's
+ * shard of a partitioned batch): output i is pair idx[i] of the n_total-pair batch. */
+EXPORT int synth_lengths_idx(int cfg, uint64_t seed, const int64_t* idx, int64_t n, int64_t n_total, int grouped,
+                             int32_t* qlen, int32_t* tlen, int32_t* h0, int n_threads) {
+    job_t j = {cfg, grouped, seed, 0, n, n_total, 0, 0, 0.0, qlen, tlen, h0, NULL, NULL, NULL, NULL, idx};
+    run_jobs(j, n_threads, len_worker);
+    return 0;
+}
+EXPORT int synth_bases_idx(int cfg, uint64_t seed, const int64_t* idx, int64_t n, int64_t n_total, int grouped,
+                           double p_n, const int64_t* q_off, const int64_t* t_off, uint8_t* q_ascii, uint8_t* t_ascii,
+                           int n_threads) {
+    job_t j = {cfg, grouped, seed, 0, n, n_total, 0, 0, p_n, NULL, NULL, NULL, q_off, t_off, q_ascii, t_ascii, idx};
+    run_jobs(j, n_threads, base_worker);
     return 0;
 }
 
@@ -268,7 +287,7 @@ EXPORT int synth_lengths(int cfg, uint64_t seed, int64_t first, int64_t n, int64
 EXPORT int synth_bases(int cfg, uint64_t seed, int64_t first, int64_t n, int64_t n_total, int grouped,
                        double p_n, const int64_t* q_off, const int64_t* t_off, uint8_t* q_ascii,
                        uint8_t* t_ascii, int n_threads) {
-    job_t j = {cfg, grouped, seed, first, n, n_total, 0, 0, p_n, NULL, NULL, NULL, q_off, t_off, q_ascii, t_ascii};
+    job_t j = {cfg, grouped, seed, first, n, n_total, 0, 0, p_n, NULL, NULL, NULL, q_off, t_off, q_ascii, t_ascii, NULL};
     run_jobs(j, n_threads, base_worker);
     return 0;
 }

@@ -18,13 +18,25 @@ def _free_port():
     return p
 
 
+def snake_reference(qlen, tlen, world):
+    """Test reference of saloba_partition's assignment (include/saloba.h): stable sort by
+    descending q*t + 2048, dealt 0..W-1, W-1..0, ...  (numpy; the product computes it on the GPU)."""
+    cost = qlen.astype(np.int64) * tlen.astype(np.int64) + 2048
+    order = np.argsort(-cost, kind="stable")
+    k = np.arange(len(cost))
+    rnd, pos = k // world, k % world
+    owner = np.empty(len(cost), np.int32)
+    owner[order] = np.where(rnd % 2 == 0, pos, world - 1 - pos)
+    return owner
+
+
 def test_partition_balance_and_coverage():
     import synth
 
     ql, tl, _ = synth.shapes(5, 200_000, grouped=True)  # worst case for an equal split
     cost = sd.pair_cost(ql, tl)
     for world in (2, 4, 8):
-        owner = sd.balanced_partition(cost, world)
+        owner = snake_reference(ql, tl, world)
         assert owner.min() == 0 and owner.max() == world - 1
         assert sd.imbalance(cost, owner, world) < 1.02
         eq = np.repeat(np.arange(world), [sd.shard_range(len(cost), world, r)[1] - sd.shard_range(len(cost), world, r)[0] for r in range(world)])
@@ -50,7 +62,7 @@ def _worker(rank, world, port, q):
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     b = synth.generate(3, 600, seed=5)
-    owner = sd.balanced_partition(sd.pair_cost(b.qlen, b.tlen), world)
+    owner = snake_reference(b.qlen, b.tlen, world)
     idx = [np.nonzero(owner == r)[0] for r in range(world)]
     mine = b.subset(idx[rank])
     s, qe, te, st, _ = oracle.align_batch(mine, threads=2)
