@@ -7,6 +7,9 @@ pinned = {}
 def alloc(name, nb):
     t = torch.empty(max(nb, 1), dtype=torch.uint8, pin_memory=True); pinned[name] = t; return t.numpy()[:nb]
 b = synth.generate(2, n, out=alloc)
+def pc(a):
+    t = torch.empty(len(a), dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True); t.numpy()[:] = a; return t.numpy()
+b = synth.Batch(b.q_ascii, pc(b.q_off), b.t_ascii, pc(b.t_off), pc(b.h0))
 dq = torch.empty(len(b.q_ascii), dtype=torch.uint8, device='cuda')
 dt = torch.empty(len(b.t_ascii), dtype=torch.uint8, device='cuda')
 for _ in range(2):
