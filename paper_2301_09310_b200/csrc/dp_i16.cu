@@ -474,6 +474,11 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : I16_MINB16) dp_i16_k
     // per subwarp: 4 spill buffers (interleaved H,F rows of 2S words) inside this block's pool slot
     constexpr int GIDX = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : G == 8 ? 3 : G == 16 ? 4 : 5;
     if (bin == LONG_BIN && *a.long_gidx != GIDX) return;  // the long bin runs at the other width
+    {   // blocks the bin cannot use exit before claiming a spill slot (empty bins: every block)
+        const int c0 = a.bin_start[bin], c1 = a.bin_start[bin + 1];
+        const int per_block = (I16_THREADS / 32) * (32 / G);  // work items one grab-round of a block takes
+        if (int64_t(blockIdx.x) * per_block >= int64_t((c1 - c0 + 1) >> 1)) return;
+    }
     const int bslot = acquire_block_slot(a.slot_bitmap, a.slot_words);
     uint32_t* const spill = reinterpret_cast<uint32_t*>(a.spill) + bslot * a.block_slot_words + (threadIdx.x / G) * 8 * S;
     __shared__ Stage<G> st;

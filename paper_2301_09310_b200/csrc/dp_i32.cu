@@ -35,6 +35,10 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
     const int k = lane & (G - 1);
     const int sub_base = lane & ~(G - 1);
     const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << sub_base);
+    {   // blocks the bin cannot use exit before claiming a spill slot (empty bins: every block)
+        const int per_block = BLOCK_THREADS / G;  // pairs one grab-round of a block takes
+        if (int64_t(blockIdx.x) * per_block >= int64_t(a.bin_start[bin + 1] - a.bin_start[bin])) return;
+    }
     const int bslot = acquire_block_slot(a.slot_bitmap, a.slot_words);
     int32_t* const spill = a.spill + bslot * a.block_slot_words + (threadIdx.x / G) * 4 * a.spill_stride;
 
