@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--force-path", type=int, default=0)
     ap.add_argument("--keep-order", type=int, default=0)
     ap.add_argument("--i16-rows", type=int, default=0)
+    ap.add_argument("--p-n", type=float, default=0.0, help="probability of N per base (real reads carry a few)")
     ap.add_argument("--grouped", action="store_true", help="config 5: components contiguous")
     ap.add_argument("--dist-backend", default="nccl", help="test hook: gloo lets several ranks share one GPU")
     return ap.parse_args()
@@ -241,12 +242,13 @@ def main():
         partition_desc = f"length-balanced snake over {world} ranks (saloba_partition), modelled max/mean {sd.imbalance(cost, owner, world):.4f}"
         total_cells_global = int(np.dot(gql.astype(np.int64), gtl.astype(np.int64)))
         counts = np.bincount(owner, minlength=world).tolist()
-        batch = synth.generate_idx(cfg, mine, n_total, seed=cfg, grouped=args.grouped, out=alloc)
+        batch = synth.generate_idx(cfg, mine, n_total, seed=cfg, grouped=args.grouped, p_n=args.p_n, out=alloc)
         del gql, gtl, owner, cost
     else:
         if world > 1:
             partition_desc = f"equal contiguous split over {world} ranks"
-        batch = synth.generate(cfg, n, seed=cfg, first=rank * n, n_total=n_total, grouped=args.grouped, out=alloc)
+        batch = synth.generate(cfg, n, seed=cfg, first=rank * n, n_total=n_total, grouped=args.grouped, p_n=args.p_n,
+                               out=alloc)
         counts = [n] * world
         total_cells_global = None
     n = batch.n  # pairs on this rank
@@ -434,7 +436,7 @@ def main():
     f_mhz = csum["sm_mhz"] or 1965.0
     bc = bins.cpu().tolist()
     lg = int(long_group.item())
-    n16, n32 = sum(bc[8:15]), sum(bc[0:8])
+    n16, n32 = sum(bc[8:15]), sum(bc[0:8])  # bin 14 = int16x2 G=1 with N in the query
     path = "int16x2" if n16 >= n32 else "int32"
     peak = sms * f_mhz * 1e6 * p_int / OPS_PER_CELL[path] / 1e9
     achieved = cells_rank / (dp_ms_avg * 1e-3) / 1e9
@@ -450,7 +452,8 @@ def main():
             "kernel": ("dp_i16_kernel" if path == "int16x2" else "dp_i32_kernel") +
                       " (all bins of one call, CUDA events on the launching stream)",
             # bin 13 = the int16x2 long bin, run at G = 2^long_group (16 or 32) this call
-            "bins": {f"{'i16' if b >= 8 else 'i32'}_G{1 << (lg if b == 13 else b % 8)}{'_long' if b == 13 else ''}": c
+            "bins": {("i16_G1_queryN" if b == 14 else
+                      f"{'i16' if b >= 8 else 'i32'}_G{1 << (lg if b == 13 else b % 8)}{'_long' if b == 13 else ''}"): c
                      for b, c in enumerate(bc) if c and b != 15},
             "dp_share_of_step": round(dp_ms_avg / ms_per_step, 3),
             "peak_derivation": f"{sms} SMs x {f_mhz:.0f} MHz (median under load) x {p_int:.0f} int lane-ops/clk/SM "

@@ -17,6 +17,11 @@ void count_launches(int n);
 // path 1 = int16x2 pair-SIMD two-pass kernel.  Bin 15 collects invalid pairs (never launched).
 constexpr int NBINS = 16;
 constexpr int BIN_SKIP = 15;
+// Bin 14: int16x2 G=1 pairs whose QUERY contains N (dp_i16_kernel<1, R, MODE, 4, QN=true>): an
+// N column's substitution is forced to `mismatch` by one LOP3 per register (the 4-entry row
+// tables have no "never matches" slot for a query code).  Target N needs no fix-up: its rows use
+// an all-mismatch table.
+constexpr int QN_BIN = 14;
 constexpr int PATH_I32 = 0, PATH_I16 = 1;
 constexpr int NGROUPS = 6;
 // Largest query block count Q = ceil(qlen/8) a bin of group size G accepts: bounds the spill pool

@@ -196,7 +196,7 @@ __device__ __forceinline__ void take_hit(uint32_t bits, int col, int rA, int rB,
     }
 }
 
-template <int G, int R, int MODE, int FMT, bool PASS2>
+template <int G, int R, int MODE, int FMT, bool PASS2, bool QN = false>
 __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned mask, const int k, const int Q,
                                               const HalfInfo& A, const HalfInfo& B,
                                               const uint32_t* __restrict__ twA, const uint32_t* __restrict__ twB,
@@ -206,6 +206,7 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                                               const int sub, const uint32_t (&twraw)[R / 4]) {
     const int al = a.alpha, be = a.beta;
     const uint32_t nbeta = pack2(-be, -be), nalpha = pack2(-al, -al), noGap = pack2(-al - be, -al - be);
+    const uint32_t mmw = pack2(a.mismatch, a.mismatch);  // QN: substitution of an N column
     uint32_t lam = 2;
     while (int(lam) < a.match + 1) lam <<= 1;
     const int rA = rowA0 + R * k, rB = rowB0 + R * k;  // my first row in each half (R rows per lane)
@@ -303,8 +304,20 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                 topF[x] = __shfl_up_sync(mask, botF[x], 1, G);
             }
         }
-        make_selectors(staged_codes<FMT>(st.q[cur][0][threadIdx.x], w, A.n),
-                       staged_codes<FMT>(st.q[cur][1][threadIdx.x], w, B.n), sel);
+        const uint32_t qcA = staged_codes<FMT>(st.q[cur][0][threadIdx.x], w, A.n);
+        const uint32_t qcB = staged_codes<FMT>(st.q[cur][1][threadIdx.x], w, B.n);
+        make_selectors(qcA, qcB, sel);
+        // QN: per column, 0xFFFF in each half whose query base is N (nibble 4); those columns take
+        // `mismatch` instead of the table byte (N never matches)
+        uint32_t nm[QN ? 8 : 1];
+        if constexpr (QN) {
+            const uint32_t vA = qcA ^ 0x44444444u, vB = qcB ^ 0x44444444u;  // N nibble -> 0
+            const uint32_t zA = ~(((vA & 0x77777777u) + 0x77777777u) | vA) & 0x88888888u;
+            const uint32_t zB = ~(((vB & 0x77777777u) + 0x77777777u) | vB) & 0x88888888u;
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+                nm[x] = (((zA >> (4 * x + 3)) & 1u) * 0xFFFFu) | (((zB >> (4 * x + 3)) & 1u) * 0xFFFF0000u);
+        }
         if (k == 0 && active) {
             // top row of the chunk: spilled row of the previous chunk, or the table boundary
             if (topA_mem) {
@@ -363,7 +376,8 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
             for (int r = 0; r < R; ++r) {
                 const uint32_t f = vaddmax(fup, nbeta, haup);
                 const uint32_t e = En[r];
-                const uint32_t sc = prmt(tabA[r], tabB[r], sel[x]);
+                uint32_t sc = prmt(tabA[r], tabB[r], sel[x]);
+                if constexpr (QN) sc = (sc & ~nm[x]) | (mmw & nm[x]);
                 uint32_t d;
                 if (MODE) {
                     // dead-zero (EXTEND): D = hdiag + s if hdiag > 0, else <= 0:
@@ -461,7 +475,7 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
     return vmax(vmax(M0, M1), vmax(M2, M3));
 }
 
-template <int G, int R, int MODE, int FMT>
+template <int G, int R, int MODE, int FMT, bool QN = false>
 __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : I16_MINB16) dp_i16_kernel(AlignArgs a, int bin) {
     // Warp-uniform control flow: a warp takes 32/G consecutive work items at once (one atomic),
     // and runs the warp-maximum of their query blocks and chunk counts; subwarps with a smaller
@@ -534,7 +548,7 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : I16_MINB16) dp_i16_k
             io.topA = io.topB = rd >= 0 ? spill + (2 * rd) * S : nullptr;
             io.bot = last ? nullptr : spill + (2 * wr) * S;
             int dummy[4];
-            uint32_t m = run_chunk<G, R, MODE, FMT, false>(a, FULL, k, Q, A, B, twA, twB, qwA, qwB, c * R * G, c * R * G,
+            uint32_t m = run_chunk<G, R, MODE, FMT, false, QN>(a, FULL, k, Q, A, B, twA, twB, qwA, qwB, c * R * G, c * R * G,
                                                         io, 0u, dummy, st, sub, twc);
 #pragma unroll
             for (int off = 1; off < G; off <<= 1) m = vmax(m, __shfl_xor_sync(FULL, m, off, G));
@@ -572,7 +586,7 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : I16_MINB16) dp_i16_k
             const uint32_t target = pack2(ckA >= 0 ? bestA : 0x7FFF, ckB >= 0 ? bestB : 0x7FFF);
             uint32_t tw2[R / 4];
             load_target_raw<R, FMT>(A, B, twA, twB, cA * R * G + R * k, cB * R * G + R * k, tw2);
-            run_chunk<G, R, MODE, FMT, true>(a, FULL, k, Q, A, B, twA, twB, qwA, qwB, cA * R * G, cB * R * G, io, target,
+            run_chunk<G, R, MODE, FMT, true, QN>(a, FULL, k, Q, A, B, twA, twB, qwA, qwB, cA * R * G, cB * R * G, io, target,
                                              hit, st, sub, tw2);
             // first hit in row-major order across the subwarp (rows grow with the lane index)
 #pragma unroll
@@ -623,6 +637,20 @@ static const void* kptr16_r(int mode, int gidx, int fmt) {
 }
 const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt, int rows) {
     return rows == 8 ? kptr16_r<8>(mode, gidx, fmt) : kptr16_r<16>(mode, gidx, fmt);
+}
+// QN variant (query contains N): G = 1, PACK4 only (2-bit sequences cannot hold N)
+const void* dp_i16_qn_kernel_ptr(int mode, int rows) {
+    if (rows == 8)
+        return mode == SALOBA_EXTEND ? (const void*)dp_i16_kernel<1, 8, 1, 4, true> : (const void*)dp_i16_kernel<1, 8, 0, 4, true>;
+    return mode == SALOBA_EXTEND ? (const void*)dp_i16_kernel<1, 16, 1, 4, true> : (const void*)dp_i16_kernel<1, 16, 0, 4, true>;
+}
+void launch_dp_i16_qn(int mode, int grid, const AlignArgs& a, cudaStream_t s) {
+    const void* fn = dp_i16_qn_kernel_ptr(mode, a.i16_rows);
+    AlignArgs args = a;
+    int bin = QN_BIN;
+    void* params[] = {&args, &bin};
+    cudaLaunchKernel(fn, dim3(grid), dim3(I16_THREADS), params, 0, s);
+    count_launches(1);
 }
 
 void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s) {

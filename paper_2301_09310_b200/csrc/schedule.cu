@@ -72,7 +72,7 @@ __host__ __device__ inline int choose_gidx_banded(int Q, int m, int w, int force
     return best;
 }
 
-__device__ inline bool i16_eligible(const ClassifyArgs& a, int64_t k, int n, int m) {
+__device__ inline int i16_eligible(const ClassifyArgs& a, int64_t k, int n, int m) {  // 0: int32, 1: int16x2, 2: int16x2 with N in the query (QN)
     const long long mn = n < m ? n : m;
     long long B = (long long)a.match * mn;
     long long lam = 1;
@@ -81,15 +81,15 @@ __device__ inline bool i16_eligible(const ClassifyArgs& a, int64_t k, int n, int
         lam = 2;
         while (lam < a.match + 1) lam <<= 1;
     }
-    if (lam * B + a.match > 32767) return false;
-    if (a.fmt == SALOBA_PACK2) return true;  // 2-bit sequences cannot hold N
+    if (lam * B + a.match > 32767) return 0;
+    if (a.fmt == SALOBA_PACK2) return 1;  // 2-bit sequences cannot hold N
     const uint32_t* w = a.q_words + a.q_word_off[k];
     const int nw = (n + 7) >> 3;
     for (int i = 0; i < nw; ++i) {
         const uint32_t v = __ldg(w + i) ^ 0x44444444u;  // nibble == 4 (N) -> zero nibble
-        if ((v - 0x11111111u) & ~v & 0x88888888u) return false;
+        if ((v - 0x11111111u) & ~v & 0x88888888u) return 2;
     }
-    return true;
+    return 1;
 }
 
 __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
@@ -115,15 +115,22 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
             key = (uint64_t(bin) << 56) | uint64_t(k);
         } else {
             const int Q = (n + 7) >> 3;
-            const int path = (a.force_path != 1 && i16_eligible(a, k, n, m)) ? PATH_I16 : PATH_I32;
+            int elig = a.force_path != 1 ? i16_eligible(a, k, n, m) : 0;
+            // query N: the QN variant exists for G = 1 only (short reads, the common case)
+            bool qn = false;
+            if (elig == 2) {
+                qn = !a.band_w && choose_gidx(Q, m, a.force_gidx, 0, a.i16_rows, true) == 0;
+                if (!qn) elig = 0;
+            }
+            const int path = elig ? PATH_I16 : PATH_I32;
             int g = path == PATH_I16 ? choose_gidx(Q, m, a.force_gidx, 0, a.i16_rows, true)
                     : a.band_w        ? choose_gidx_banded(Q, m, a.band_w[k], a.force_gidx)
-                                      : choose_gidx(Q, m, a.force_gidx, 0, I32_ROWS, false);
+                                      : choose_gidx(Q, m, a.force_gidx, 1, I32_ROWS, false);  // int32 G=1 measured 3x slower than G=2
             if (path == PATH_I16 && a.force_gidx < 0 && g >= NGROUPS - 2) {
                 g = NGROUPS - 1;  // the long bin: G=16 or G=32 decided once it is counted
                 atomicMax(a.long_qmax, Q);
             }
-            bin = path * 8 + g;
+            bin = qn ? QN_BIN : path * 8 + g;
             if (a.keep_order)
                 key = (uint64_t(bin) << 56) | uint64_t(k);
             else

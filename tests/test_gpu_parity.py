@@ -324,3 +324,17 @@ def test_host_context_reuse_offsets_and_errors(sb):
     with pytest.raises(sb.SalobaError):
         sb.align_host(big, sb.BWA_MEM, sb.LOCAL, ctx=ctx)
     ctx.close()
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_query_n_bin(sb, mode):
+    """Reads with N in the query run on the int16x2 G=1 QN variant (bin 14: an N column's
+    substitution forced to mismatch), bit-exact vs the oracle; N in the target only needs no bin."""
+    import torch
+
+    b = synth.generate(2, 20_000, seed=41, p_n=0.002)
+    bins = torch.zeros(16, dtype=torch.int32, device="cuda")
+    got = gpu_align(sb, b, sb.BWA_MEM, mode, sb.Options(bin_counts=bins))
+    bc = bins.cpu().tolist()
+    assert bc[14] > 1000 and bc[8] > 1000 and sum(bc[0:8]) == 0, bc
+    assert_same(got, oracle_align(b, sb.BWA_MEM, mode), b, f"query-N bin mode={mode}")
