@@ -338,3 +338,30 @@ def test_query_n_bin(sb, mode):
     bc = bins.cpu().tolist()
     assert bc[14] > 1000 and bc[8] > 1000 and sum(bc[0:8]) == 0, bc
     assert_same(got, oracle_align(b, sb.BWA_MEM, mode), b, f"query-N bin mode={mode}")
+
+
+def test_long_identical_pair_closed_form(sb):
+    """Maximum-size direction: one 50 kbp identical pair (score beyond int16 -> int32 long bin,
+    2.5e9 cells on one subwarp) against the closed form (L, L-1, L-1); EXTEND adds h0."""
+    rng = np.random.default_rng(50)
+    L = 50_000
+    q = "".join(rng.choice(list("ACGT"), L))
+    b = synth.from_pairs([(q, q), ("ACGT", "ACGT")], np.array([5, 5], np.int32))
+    got = gpu_align(sb, b, sb.BWA_MEM, 0)
+    assert got[3] == -1 and (got[0][0], got[1][0], got[2][0]) == (L, L - 1, L - 1)
+    got = gpu_align(sb, b, sb.BWA_MEM, 1)
+    assert got[3] == -1 and (got[0][0], got[1][0], got[2][0]) == (L + 5, L - 1, L - 1)
+
+
+def test_length_beyond_envelope_is_invalid(sb):
+    """Lengths > 2^20 (the S:151 int32 envelope) are invalid data: status = first such pair."""
+    import torch
+
+    big = "A" * ((1 << 20) + 1)
+    b = synth.from_pairs([("ACGT", "ACGT"), ("ACGT", big), ("AC", "AC")])
+    d = "cuda"
+    qa, qo = torch.from_numpy(b.q_ascii).to(d), torch.from_numpy(b.q_off).to(d)
+    ta, to = torch.from_numpy(b.t_ascii).to(d), torch.from_numpy(b.t_off).to(d)
+    s, qe, te, st, qst, tst = sb.align(qa, qo, ta, to, max_qlen=64)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 1 and s.cpu().tolist() == [4, -1, 2]
