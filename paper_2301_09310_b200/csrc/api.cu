@@ -21,7 +21,7 @@ size_t cub_sort_temp_bytes(int64_t n);
 void launch_status_init(int64_t* st, cudaStream_t s);
 void launch_status_final(int64_t* st, cudaStream_t s);
 void launch_dp_i32(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s);
-const void* dp_i32_kernel_ptr(int mode, int gidx, bool band);
+const void* dp_i32_kernel_ptr(int mode, int gidx, bool band, bool fast);
 void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s);
 const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt, int rows);
 const void* dp_i16_qn_kernel_ptr(int mode, int rows);
@@ -61,10 +61,14 @@ static const DevInfo* dev_info(int device) {
         cudaSetDevice(device);
         for (int mode = 0; mode < 2; ++mode)
             for (int g = 0; g < NGROUPS; ++g) {
-                int nb = 0, nbb = 0;  // plain and banded (NEXT-2) int32 kernels
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i32_kernel_ptr(mode, g, false), BLOCK_THREADS, 0);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, dp_i32_kernel_ptr(mode, g, true), BLOCK_THREADS, 0);
-                d.blocks_i32[mode][g] = std::max(1, std::max(nb, nbb));
+                int nb = 1;  // max over the plain / banded (NEXT-2) / FAST int32 variants
+                for (int v = 0; v < 4; ++v) {
+                    int x = 0;
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, dp_i32_kernel_ptr(mode, g, v & 1, v >> 1),
+                                                                  BLOCK_THREADS, 0);
+                    nb = std::max(nb, x);
+                }
+                d.blocks_i32[mode][g] = nb;
                 for (int ri = 0; ri < 2; ++ri) {
                     nb = 0;
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i16_kernel_ptr(mode, g, SALOBA_PACK4, ri ? 16 : 8),
@@ -241,9 +245,10 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
               reinterpret_cast<uint32_t*>(ws + L.vals_in), reinterpret_cast<uint32_t*>(ws + L.vals_out),
               ws + L.cub, L.cub_bytes};
     const int i16_rows = o.i16_rows == 8 ? 8 : I16_ROWS_DEFAULT;
+    const int i32_fast = (sc.match <= 127 && sc.mismatch >= -128) ? 1 : 0;  // int8 substitution tables
     ClassifyArgs ca{q_words, q_word_off, int(fmt), sc.match, q_len, t_len, h0, n_pairs, int(mode), force_g,
                     band_w ? 1 : o.force_path, o.keep_order, i16_rows, Qsup * 8, score, q_end, t_end, kv.keys_in,
-                    kv.vals_in, bin_count, (unsigned long long*)status, long_qmax, band_w};
+                    kv.vals_in, bin_count, (unsigned long long*)status, long_qmax, band_w, i32_fast};
     const int64_t cap16 = int64_t(grid_for(d, int(mode), PATH_I16, NGROUPS - 2, i16_rows)) * (I16_THREADS / 16) * 2;
     if (run_classify_sort(ca, kv, bin_start, d->sms, long_gidx, cap16, s) != cudaSuccess) return SALOBA_ECUDA;
 
@@ -263,6 +268,7 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
         a.i16_rows = i16_rows;
         a.long_gidx = long_gidx;
         a.band_w = band_w;
+        a.i32_fast = i32_fast;
         if (o.bin_counts) cudaMemcpyAsync(o.bin_counts, bin_count, NBINS * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
         if (o.long_group) cudaMemcpyAsync(o.long_group, long_gidx, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
         if (o.ev_dp_begin) cudaEventRecord((cudaEvent_t)o.ev_dp_begin, s);
@@ -290,6 +296,11 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
                 else
                     launch_dp_i32(int(mode), g, grid_for(d, int(mode), path, g), a, path * 8 + g, as);
             }
+        {   // int32 wide bin (values may reach 2^28, or scores beyond int8): the plain kernel, G = 32
+            a.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(NGROUPS - 1), Qsup) + 8;
+            launch_dp_i32(int(mode), NGROUPS - 1, grid_for(d, int(mode), PATH_I32, NGROUPS - 1), a, I32_WIDE_BIN,
+                          aux[(j + 1) % NAUX]);
+        }
         if (fmt == SALOBA_PACK4) {  // QN bin: int16x2 G=1 pairs whose query contains N
             a.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(0), Qsup) + 8;
             launch_dp_i16_qn(int(mode), d->sms * d->blocks_i16qn[i16_rows == 8 ? 0 : 1][int(mode)], a,

@@ -22,6 +22,10 @@ constexpr int BIN_SKIP = 15;
 // tables have no "never matches" slot for a query code).  Target N needs no fix-up: its rows use
 // an all-mismatch table.
 constexpr int QN_BIN = 14;
+// Bin 7: int32 pairs whose values could reach 2^28 (the packed best-cell keys of the FAST int32
+// kernel would overflow) or every int32 pair of a call whose scores do not fit int8; runs the plain
+// int32 kernel at G = 32.
+constexpr int I32_WIDE_BIN = 7;
 constexpr int PATH_I32 = 0, PATH_I16 = 1;
 constexpr int NGROUPS = 6;
 // Largest query block count Q = ceil(qlen/8) a bin of group size G accepts: bounds the spill pool
@@ -70,6 +74,7 @@ struct ClassifyArgs {
     unsigned long long* status;
     int32_t* long_qmax;  // max Q (8-base blocks) of the int16x2 long bin (atomicMax)
     const int32_t* band_w;  // NEXT-2: per-pair band half-width, or nullptr (banded pairs take the int32 path)
+    int32_t i32_fast;       // 1: int32 pairs below the 2^28 value bound go to the FAST kernels (bins 0..5)
 };
 
 // Queries of >= LONG_Q blocks take the int16x2 "long bin" (bin PATH_I16*8 + NGROUPS-1); its width
@@ -103,6 +108,7 @@ struct AlignArgs {
     int32_t i16_rows;         // target rows per lane of the int16x2 kernel (8 or 16)
     const int32_t* long_gidx; // group index that runs LONG_BIN (set by bin_scan_kernel); others exit
     const int32_t* band_w;    // NEXT-2: per-pair band half-width (cells |i-j| <= w), or nullptr
+    int32_t i32_fast;         // 1: the call's scores fit int8 (FAST int32 kernels in bins 0..5)
 };
 
 // 8 consecutive bases [8w, 8w+8) of a packed sequence as 8 nibbles (base c in nibble c).

@@ -29,7 +29,20 @@
 
 namespace saloba {
 
-template <int G, int MODE, bool BAND>
+__device__ __forceinline__ uint32_t prmt32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// FAST (every call whose scores fit int8; pairs whose values could reach 2^28 go to bin 7, which
+// runs FAST = false): the substitution is one PRMT from a per-row int8 table over the query codes,
+// sign-extended to 32 bits (query N / padding select the second source, a `mismatch` byte); the
+// EXTEND dead-zero rule is min(hdiag + s, lambda*hdiag) (one VIADDMNMX, lambda = 2^k >= match+1,
+// as in dp_i16.cu); and the per-row best is tracked per step on packed keys h*8 + (7 - x) (one
+// 3-input max per two cells, then one compare per row per step) instead of compare + 2 selects
+// per cell.  Same results: max h, first (smallest) column within the row.
+template <int G, int MODE, bool BAND, bool FAST>
 __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int bin) {
     const int lane = threadIdx.x & 31;
     const int k = lane & (G - 1);
@@ -71,11 +84,17 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
             // target codes of my 8 rows; rows past m and N never match (0xFF)
             const uint32_t tword = (strip < strips) ? load_block8(tw, strip, a.fmt) : 0u;
             int tc[8];
+            uint32_t tab[FAST ? 8 : 1];  // FAST: int8 scores of row r against query codes 0..3
+            const uint32_t mmb = (uint32_t(mm) & 0xFFu) * 0x01010101u;
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
                 const int code = nib(tword, r);
                 tc[r] = (r0 + r < m && code < 4) ? code : 0xFF;
+                if constexpr (FAST)
+                    tab[r] = tc[r] == 0xFF ? mmb : mmb ^ (((uint32_t(ma) ^ uint32_t(mm)) & 0xFFu) << (8 * tc[r]));
             }
+            uint32_t lam = 2;
+            while (int(lam) < ma + 1) lam <<= 1;
             int Hl[8], El[8], bv[8], bc[8];
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
@@ -147,8 +166,19 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                     // BAND: does this block cross the band edge? (then cells are masked)
                     const bool edge = BAND && ((r0 + 7) - 8 * w > wb || (8 * w + 7) - r0 > wb);
                     int qc[8];
+                    uint32_t sel[FAST ? 8 : 1];
 #pragma unroll
-                    for (int x = 0; x < 8; ++x) qc[x] = (8 * w + x < n) ? nib(qword, x) : 15;
+                    for (int x = 0; x < 8; ++x) {
+                        qc[x] = (8 * w + x < n) ? nib(qword, x) : 15;
+                        if constexpr (FAST) {
+                            const uint32_t cx = qc[x] < 4 ? uint32_t(qc[x]) : 4u;  // N / padding -> mismatch byte
+                            sel[x] = cx * 0x1111u | 0x8880u;                      // [c, sign, sign, sign]
+                        }
+                    }
+                    int smax[FAST ? 8 : 1];  // FAST: per-row max of h*8 + (7 - x) over this step
+#pragma unroll
+                    for (int r = 0; r < (FAST ? 8 : 1); ++r) smax[r] = -1;
+                    int kprev[FAST ? 8 : 1];
 #pragma unroll
                     for (int x = 0; x < 8; ++x) {
                         int hup = topH[x], fup = topF[x];
@@ -158,12 +188,22 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                         for (int r = 0; r < 8; ++r) {
                             const int e = max(Hl[r] - al, El[r] - be);
                             const int f = max(hup - al, fup - be);
-                            int d = hdiag + ((tc[r] == qc[x]) ? ma : mm);
-                            if (MODE) d = (hdiag > 0) ? d : 0;
+                            int d;
+                            if constexpr (FAST) {
+                                const int sc = int(prmt32(tab[r], mmb, sel[x]));
+                                d = MODE ? min(hdiag + sc, hdiag * int(lam)) : hdiag + sc;
+                            } else {
+                                d = hdiag + ((tc[r] == qc[x]) ? ma : mm);
+                                if (MODE) d = (hdiag > 0) ? d : 0;
+                            }
                             int h = max(max(0, e), max(f, d));
                             int ee = e, ff = f;
                             if (BAND && edge && abs(r0 + r - col) > wb) h = ee = ff = 0;  // outside the band
-                            if (h > bv[r]) {
+                            if constexpr (FAST) {
+                                const int key = h * 8 + (7 - x);
+                                if (x & 1) smax[r] = max(smax[r], max(kprev[r], key));
+                                else kprev[r] = key;
+                            } else if (h > bv[r]) {
                                 bv[r] = h;
                                 bc[r] = col;
                             }
@@ -175,6 +215,14 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                         }
                         botH[x] = hup;
                         botF[x] = fup;
+                    }
+                    if constexpr (FAST) {
+#pragma unroll
+                        for (int r = 0; r < 8; ++r)
+                            if ((smax[r] >> 3) > bv[r]) {
+                                bv[r] = smax[r] >> 3;
+                                bc[r] = 8 * w + 7 - (smax[r] & 7);
+                            }
                     }
                     corner = topH[7];
                     if (k == G - 1 && c + 1 < chunks) {
@@ -225,24 +273,29 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
     release_block_slot(a.slot_bitmap, bslot);
 }
 
-template <int MODE, bool BAND>
+template <int MODE, bool BAND, bool FAST>
 static const void* kptr_mode(int gidx) {
     switch (gidx) {
-    case 0: return (const void*)dp_i32_kernel<1, MODE, BAND>;
-    case 1: return (const void*)dp_i32_kernel<2, MODE, BAND>;
-    case 2: return (const void*)dp_i32_kernel<4, MODE, BAND>;
-    case 3: return (const void*)dp_i32_kernel<8, MODE, BAND>;
-    case 4: return (const void*)dp_i32_kernel<16, MODE, BAND>;
-    default: return (const void*)dp_i32_kernel<32, MODE, BAND>;
+    case 0: return (const void*)dp_i32_kernel<1, MODE, BAND, FAST>;
+    case 1: return (const void*)dp_i32_kernel<2, MODE, BAND, FAST>;
+    case 2: return (const void*)dp_i32_kernel<4, MODE, BAND, FAST>;
+    case 3: return (const void*)dp_i32_kernel<8, MODE, BAND, FAST>;
+    case 4: return (const void*)dp_i32_kernel<16, MODE, BAND, FAST>;
+    default: return (const void*)dp_i32_kernel<32, MODE, BAND, FAST>;
     }
 }
-const void* dp_i32_kernel_ptr(int mode, int gidx, bool band) {
-    if (band) return mode == SALOBA_EXTEND ? kptr_mode<1, true>(gidx) : kptr_mode<0, true>(gidx);
-    return mode == SALOBA_EXTEND ? kptr_mode<1, false>(gidx) : kptr_mode<0, false>(gidx);
+template <bool FAST>
+static const void* kptr_fast(int mode, int gidx, bool band) {
+    if (band) return mode == SALOBA_EXTEND ? kptr_mode<1, true, FAST>(gidx) : kptr_mode<0, true, FAST>(gidx);
+    return mode == SALOBA_EXTEND ? kptr_mode<1, false, FAST>(gidx) : kptr_mode<0, false, FAST>(gidx);
+}
+const void* dp_i32_kernel_ptr(int mode, int gidx, bool band, bool fast) {
+    return fast ? kptr_fast<true>(mode, gidx, band) : kptr_fast<false>(mode, gidx, band);
 }
 
 void launch_dp_i32(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s) {
-    const void* fn = dp_i32_kernel_ptr(mode, gidx, a.band_w != nullptr);
+    // bins 0..5: FAST when the call's scores fit int8; bin I32_WIDE_BIN (G = 32): the plain kernel
+    const void* fn = dp_i32_kernel_ptr(mode, gidx, a.band_w != nullptr, bin != I32_WIDE_BIN && a.i32_fast);
     AlignArgs args = a;
     void* params[] = {&args, &bin};
     cudaLaunchKernel(fn, dim3(grid), dim3(BLOCK_THREADS), params, 0, s);

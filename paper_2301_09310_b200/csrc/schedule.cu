@@ -131,6 +131,17 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
                 atomicMax(a.long_qmax, Q);
             }
             bin = qn ? QN_BIN : path * 8 + g;
+            if (path == PATH_I32) {
+                // FAST int32 kernels pack h*8 + column keys and form lambda*H: values must stay < 2^27
+                const long long mn = n < m ? n : m;
+                long long B = (long long)a.match * mn, lam = 1;
+                if (a.mode == SALOBA_EXTEND) {
+                    B += a.h0[k];
+                    lam = 2;
+                    while (lam < a.match + 1) lam <<= 1;
+                }
+                if (!a.i32_fast || lam * B + a.match >= (1ll << 27)) bin = I32_WIDE_BIN;
+            }
             if (a.keep_order)
                 key = (uint64_t(bin) << 56) | uint64_t(k);
             else
