@@ -139,8 +139,8 @@ static Layout layout(int64_t n, size_t spill_bytes) {
     Layout L{};
     size_t off = 0;
     const size_t nn = size_t(std::max<int64_t>(n, 1));
-    L.keys_in = off; off = align_up(off + nn * 8, 256);
-    L.keys_out = off; off = align_up(off + nn * 8, 256);
+    L.keys_in = off; off = align_up(off + nn * 4, 256);
+    L.keys_out = off; off = align_up(off + nn * 4, 256);
     L.vals_in = off; off = align_up(off + nn * 4, 256);
     L.vals_out = off; off = align_up(off + nn * 4, 256);
     L.cub_bytes = cub_sort_temp_bytes(n);
@@ -241,7 +241,7 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
     if (cudaMemsetAsync(small, 0, 1024, s) != cudaSuccess) return SALOBA_ECUDA;
     launch_status_init(status, s);
 
-    SortKV kv{reinterpret_cast<uint64_t*>(ws + L.keys_in), reinterpret_cast<uint64_t*>(ws + L.keys_out),
+    SortKV kv{reinterpret_cast<uint32_t*>(ws + L.keys_in), reinterpret_cast<uint32_t*>(ws + L.keys_out),
               reinterpret_cast<uint32_t*>(ws + L.vals_in), reinterpret_cast<uint32_t*>(ws + L.vals_out),
               ws + L.cub, L.cub_bytes};
     const int i16_rows = o.i16_rows == 8 ? 8 : I16_ROWS_DEFAULT;

@@ -42,8 +42,8 @@ constexpr int I16_ROWS_DEFAULT = 16;
 constexpr int I32_ROWS = 8;
 
 struct SortKV {
-    uint64_t* keys_in;
-    uint64_t* keys_out;
+    uint32_t* keys_in;
+    uint32_t* keys_out;
     uint32_t* vals_in;
     uint32_t* vals_out;
     void* cub_temp;
@@ -68,7 +68,7 @@ struct ClassifyArgs {
     int32_t* score;
     int32_t* q_end;
     int32_t* t_end;
-    uint64_t* keys;
+    uint32_t* keys;
     uint32_t* vals;
     int32_t* bin_count;  // [NBINS]
     unsigned long long* status;

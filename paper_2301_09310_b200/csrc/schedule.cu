@@ -3,8 +3,9 @@
 // approximate sorting").
 //
 // Per pair: validate, pick the precision path and the subwarp size G from a lane-step cost model
-// (the Q+G-1 ramp of SPEC S:262-279 plus a per-chunk-boundary spill term), then build a 64-bit
-// sort key  [bin:8][~Q:24][~tlen:32]  so that one CUB radix sort groups each bin contiguously,
+// (the Q+G-1 ramp of SPEC S:262-279 plus a per-chunk-boundary spill term), then build a 32-bit
+// sort key  [bin:4][~min(Q,16383):14][~min(tlen,16383):14]  so that one stable CUB radix sort
+// (4 passes; 64-bit keys took 8) groups each bin contiguously,
 // longest queries first (LPT order for the persistent kernels' dynamic work queues), and places
 // pairs of near-identical shape next to each other (the int16x2 path packs neighbours).
 #include <cub/device/device_radix_sort.cuh>
@@ -105,14 +106,14 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
             ok = ok && h >= 1 && h <= MAX_H0;
         }
         int bin;
-        uint64_t key;
+        uint32_t key;
         if (!ok) {
             bin = BIN_SKIP;
             a.score[k] = -1;
             a.q_end[k] = -2;
             a.t_end[k] = -2;
             atomicMin(a.status, (unsigned long long)k);
-            key = (uint64_t(bin) << 56) | uint64_t(k);
+            key = uint32_t(bin) << 28;
         } else {
             const int Q = (n + 7) >> 3;
             int elig = a.force_path != 1 ? i16_eligible(a, k, n, m) : 0;
@@ -143,10 +144,10 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
                 if (!a.i32_fast || lam * B + a.match >= (1ll << 27)) bin = I32_WIDE_BIN;
             }
             if (a.keep_order)
-                key = (uint64_t(bin) << 56) | uint64_t(k);
+                key = uint32_t(bin) << 28;  // stable sort: input order inside the bin
             else
-                key = (uint64_t(bin) << 56) | (uint64_t(0xFFFFFFu - uint32_t(min(Q, 0xFFFFFF))) << 32) |
-                      uint64_t(0xFFFFFFFFu - uint32_t(m));
+                key = (uint32_t(bin) << 28) | ((16383u - uint32_t(min(Q, 16383))) << 14) |
+                      (16383u - uint32_t(min(m, 16383)));  // longest query, then target, first
         }
         a.keys[k] = key;
         a.vals[k] = uint32_t(k);
@@ -177,8 +178,8 @@ __global__ void bin_scan_kernel(const int32_t* count, int32_t* start, const int3
 
 size_t cub_sort_temp_bytes(int64_t n) {
     size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
-                                    (uint32_t*)nullptr, int(n > 0 ? n : 1), 0, 64);
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, int(n > 0 ? n : 1), 0, 32);
     return bytes;
 }
 
@@ -191,7 +192,7 @@ cudaError_t run_classify_sort(const ClassifyArgs& ca, const SortKV& kv, int32_t*
         count_launches(1);
         size_t tb = kv.cub_temp_bytes;
         cudaError_t e = cub::DeviceRadixSort::SortPairs(kv.cub_temp, tb, kv.keys_in, kv.keys_out, kv.vals_in,
-                                                        kv.vals_out, int(ca.n), 0, 64, s);
+                                                        kv.vals_out, int(ca.n), 0, 32, s);
         if (e != cudaSuccess) return e;
     }
     bin_scan_kernel<<<1, 32, 0, s>>>(ca.bin_count, bin_start, ca.long_qmax, long_gidx, cap16, ca.force_gidx);
