@@ -36,7 +36,10 @@ __host__ __device__ constexpr int qmax_for_gidx(int gidx) {
 constexpr int MAX_LEN = 1 << 20;   // S:151 overflow envelope for int32 cells
 constexpr int MAX_H0 = 1 << 29;
 constexpr int BLOCK_THREADS = 256;
-constexpr int I16_THREADS = 128;
+#ifndef I16_BLOCK
+#define I16_BLOCK 128
+#endif
+constexpr int I16_THREADS = I16_BLOCK;
 // target rows per lane (strip height) of the int16x2 kernel: 16 = two packed target words
 constexpr int I16_ROWS_DEFAULT = 16;
 constexpr int I32_ROWS = 8;

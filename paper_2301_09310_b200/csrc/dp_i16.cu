@@ -476,7 +476,7 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
 }
 
 template <int G, int R, int MODE, int FMT, bool QN = false>
-__global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 : I16_MINB16) dp_i16_kernel(AlignArgs a, int bin) {
+__global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 * 128 / I16_THREADS : I16_MINB16) dp_i16_kernel(AlignArgs a, int bin) {
     // Warp-uniform control flow: a warp takes 32/G consecutive work items at once (one atomic),
     // and runs the warp-maximum of their query blocks and chunk counts; subwarps with a smaller
     // item compute padding (harmless by the dominance argument above).  Shuffles can then use the
