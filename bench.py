@@ -38,8 +38,11 @@ WORKLOADS = {
 # Minimal ALU-pipe instructions per cell.  Per register the update needs 3 max-type
 # ops (E, F, H), the substitution lookup (PRMT) and half a running-max op: 4.5 ALU-only
 # instructions (max/min/PRMT have no FMA-pipe form on sm_100a; the two adds go to the FMA pipe).
-# int16x2 registers carry 2 cells -> 2.25 ALU ops per cell; int32 -> 4.5.
-OPS_PER_CELL = {"int32": 4.5, "int16x2": 2.25}
+# int16x2 registers carry 2 cells -> 2.25 ALU ops per cell; int32 -> 4.5.  EXTEND adds the
+# dead-zero rule of its definition (D = H(i-1,j-1) + S only if H(i-1,j-1) > 0): one
+# more min-type op per register, D = min(hdiag + s, lambda*hdiag) -> 5.5 per register, 2.75 per cell.
+OPS_PER_CELL = {("int32", "local"): 4.5, ("int16x2", "local"): 2.25,
+                ("int32", "extend"): 5.5, ("int16x2", "extend"): 2.75}
 
 
 def parse():
@@ -438,7 +441,8 @@ def main():
     lg = int(long_group.item())
     n16, n32 = sum(bc[8:15]), sum(bc[0:8])  # bin 14 = int16x2 G=1 with N in the query
     path = "int16x2" if n16 >= n32 else "int32"
-    peak = sms * f_mhz * 1e6 * p_int / OPS_PER_CELL[path] / 1e9
+    opc = OPS_PER_CELL[(path, args.mode)]
+    peak = sms * f_mhz * 1e6 * p_int / opc / 1e9
     achieved = cells_rank / (dp_ms_avg * 1e-3) / 1e9
     traffic = None
     try:  # DRAM bytes per launch of the dominant kernel from the committed ncu capture of this command
@@ -457,7 +461,7 @@ def main():
                      for b, c in enumerate(bc) if c and b != 15},
             "dp_share_of_step": round(dp_ms_avg / ms_per_step, 3),
             "peak_derivation": f"{sms} SMs x {f_mhz:.0f} MHz (median under load) x {p_int:.0f} int lane-ops/clk/SM "
-                               f"[{p_src}] / {OPS_PER_CELL[path]} ALU ops per cell ({path} path)"}
+                               f"[{p_src}] / {opc} ALU ops per cell ({path} path, {args.mode} mode)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(batch, mode, args.cpu_seconds)
