@@ -263,6 +263,122 @@ __global__ void __launch_bounds__(256) pack_tile_kernel(const uint8_t* __restric
     }
 }
 
+// Tile sweep v2 (the default): per warp, the tile's per-sequence data (exclusive word counts,
+// byte and word offsets relative to the tile, lengths) is staged in shared memory; each lane packs
+// U consecutive words of the tile's flattened word list (one binary search per lane, then a
+// forward walk across sequence ends), so a warp reads ~1 KB of contiguous ASCII per iteration and
+// addresses are 32-bit offsets from the tile base.  Partial last words are masked branch-free.
+template <int BITS>
+__global__ void __launch_bounds__(256) pack_tile2_kernel(const uint8_t* __restrict__ ascii,
+                                                         const int64_t* __restrict__ byte_off, int64_t n_seqs,
+                                                         int64_t base, uint32_t* __restrict__ words,
+                                                         int64_t* __restrict__ word_off, int32_t* __restrict__ lens,
+                                                         unsigned long long* __restrict__ status) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int B = 32 / BITS;  // bases per word
+    constexpr int U = 4;          // consecutive words per lane per iteration
+    __shared__ uint8_t lut[256];
+    __shared__ int s_ex[8][33], s_b0[8][32], s_len[8][32], s_w0[8][32];
+    build_lut(lut, BITS);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t total = byte_off[n_seqs];
+    const int64_t tiles = (n_seqs + 31) / 32;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
+    for (int64_t tile = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; tile < tiles; tile += warps) {
+        const int64_t s = tile * 32 + lane;
+        const bool has = s < n_seqs;
+        const int64_t b0 = has ? byte_off[s] : byte_off[n_seqs];
+        const int len = has ? int(byte_off[s + 1] - b0) : 0;
+        const int64_t w0 = b0 / B + s + base;
+        if (has) {
+            word_off[s] = w0;
+            if (lens) lens[s] = len;
+            if (s == n_seqs - 1) word_off[n_seqs] = byte_off[n_seqs] / B + n_seqs + base;
+        }
+        const int nw = (len + B - 1) / B;
+        int incl = nw;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const int tot = __shfl_sync(FULL, incl, 31);
+        const int64_t tb0 = __shfl_sync(FULL, b0, 0), tw0 = __shfl_sync(FULL, w0, 0);
+        s_ex[wid][lane] = incl - nw;
+        if (lane == 31) s_ex[wid][32] = incl;
+        s_b0[wid][lane] = int(b0 - tb0);
+        s_len[wid][lane] = len;
+        s_w0[wid][lane] = int(w0 - tw0);
+        __syncwarp();
+        const uint8_t* abase = ascii + tb0;
+        uint32_t* wbase = words + tw0;
+        for (int j0 = 0; j0 < tot; j0 += 32 * U) {
+            const int j = j0 + lane * U;
+            if (j < tot) {
+                int own = 0;  // last sequence whose first flattened word is <= j
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1)
+                    if (own + step <= 31 && s_ex[wid][own + step] <= j) own += step;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int jj = j + u;
+                    if (jj >= tot) break;
+                    while (s_ex[wid][own + 1] <= jj) ++own;  // crossed a sequence end
+                    const int w = jj - s_ex[wid][own];
+                    const int rb = s_b0[wid][own] + w * B;  // first byte of this word (tile-relative)
+                    const int olen = s_len[wid][own];
+                    const int nv = min(B, olen - w * B);     // valid bases in this word (>= 1)
+                    uint32_t out = 0, bad = 0;
+                    bool fast = false;
+                    const uint2 by0 = load8(ascii, tb0 + rb, total);  // absolute: keeps the 4-byte alignment
+                    if (BITS == 4) {
+                        // bases past the sequence end read as 'A' for the check, become padding nibbles
+                        const uint32_t klo = nv >= 4 ? 0xFFFFFFFFu : (1u << (8 * nv)) - 1u;
+                        const uint32_t khi = nv >= 8 ? 0xFFFFFFFFu : nv <= 4 ? 0u : (1u << (8 * (nv - 4))) - 1u;
+                        const uint2 by = make_uint2((by0.x & klo) | (0x41414141u & ~klo), (by0.y & khi) | (0x41414141u & ~khi));
+                        uint32_t n0 = 0;
+                        fast = fast_acgt8(by, n0);
+                        out = nv >= 8 ? n0 : (n0 | (0xFFFFFFFFu << (4 * nv)));
+                    } else if (nv == B) {
+                        uint32_t n0 = 0, n1 = 0;
+                        fast = fast_acgt8(by0, n0) && fast_acgt8(load8(ascii, tb0 + rb + 8, total), n1);
+                        uint32_t a = n0, b = n1;  // 16 nibbles (each <= 3) -> 16 two-bit fields
+                        a = (a | (a >> 2)) & 0x0F0F0F0Fu; a = (a | (a >> 4)) & 0x00FF00FFu; a = (a | (a >> 8)) & 0xFFFFu;
+                        b = (b | (b >> 2)) & 0x0F0F0F0Fu; b = (b | (b >> 4)) & 0x00FF00FFu; b = (b | (b >> 8)) & 0xFFFFu;
+                        out = a | (b << 16);
+                    }
+                    if (!fast) {  // U, N (PACK4), lower-case-free table path, invalid bytes
+                        out = 0;
+#pragma unroll
+                        for (int half = 0; half < B / 8; ++half) {
+                            const uint2 by = half == 0 ? by0 : load8(ascii, tb0 + rb + 8, total);
+                            const int nvalid = min(8, nv - half * 8);
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) {
+                                const uint32_t byte = ((c < 4 ? by.x : by.y) >> (8 * (c & 3))) & 0xFFu;
+                                uint32_t code = lut[byte];
+                                if (c < nvalid) bad |= code;
+                                if (c >= nvalid || code == 0xFFu) code = BITS == 4 ? 15u : 0u;
+                                out |= code << (BITS * (half * 8 + c));
+                            }
+                        }
+                    }
+                    wbase[s_w0[wid][own] + w] = out;
+                    if (bad & 0x80u) {
+                        for (int c = 0; c < nv; ++c)
+                            if (lut[abase[rb + c]] == 0xFF) {
+                                atomicMin(status, (unsigned long long)(tb0 + rb + c));
+                                break;
+                            }
+                    }
+                }
+            }
+        }
+        __syncwarp();  // the next tile overwrites this warp's staging
+    }
+}
+
 __global__ void status_init(unsigned long long* st) { *st = ~0ull >> 1; }
 __global__ void status_final(unsigned long long* st) {
     if (*st == (~0ull >> 1)) *st = (unsigned long long)(-1ll);
@@ -296,7 +412,7 @@ void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n,
             else
                 pack_kernel<2><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
                                                     (unsigned long long*)status);
-        } else {
+        } else if (getenv("SALOBA_PACK_TILE1") != nullptr) {  // A/B: the first tile sweep
             const int64_t need = (n + 255) / 256;  // one warp per 32-sequence tile, 8 warps per block
             const int grid = int(need < g8 ? need : g8);
             if (fmt == SALOBA_PACK4)
@@ -305,6 +421,15 @@ void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n,
             else
                 pack_tile_kernel<2><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
                                                          (unsigned long long*)status);
+        } else {
+            const int64_t need = (n + 255) / 256;  // one warp per 32-sequence tile, 8 warps per block
+            const int grid = int(need < g8 ? need : g8);
+            if (fmt == SALOBA_PACK4)
+                pack_tile2_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
+                                                          (unsigned long long*)status);
+            else
+                pack_tile2_kernel<2><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
+                                                          (unsigned long long*)status);
         }
         count_launches(1);
     }
