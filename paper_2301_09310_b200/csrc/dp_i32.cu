@@ -159,6 +159,10 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                     if (w >= 0) corner = topH[7];
 #pragma unroll
                     for (int x = 0; x < 8; ++x) botH[x] = botF[x] = 0;
+                    if (w >= 0 && w < blo) {  // left of my band: the column left of block blo is out of
+#pragma unroll                                 // band (H = E = 0), not the column -1 boundary
+                        for (int r = 0; r < 8; ++r) Hl[r] = El[r] = 0;
+                    }
                     continue;
                 }
                 if (w >= 0 && w < Q && r0 < m) {

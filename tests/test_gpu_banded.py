@@ -134,3 +134,17 @@ def test_banded_long_reads_sampled(sb, mode):
     sub = b.subset(idx)
     ref = oracle_banded(sub, w[idx], sb.BWA_MEM, mode)
     assert_same(tuple(x[idx] for x in got[:3]), ref, sub, w[idx], f"config4 banded mode={mode}")
+
+
+def test_banded_extend_large_h0_band_left_edge(sb):
+    """EXTEND with large h0 and bands whose left edge falls exactly on a block boundary: the first
+    in-band cell of a strip must see an out-of-band (zero) left neighbour, not the H(i,-1)
+    boundary of column -1 (a stale-boundary bug would show up here)."""
+    rng = np.random.default_rng(88)
+    b = synth.random_pairs(3000, 20, 120, seed=88, p_mut=0.05)
+    b.h0[:] = rng.integers(40, 120, b.n).astype(np.int32)
+    w = rng.choice(np.array([0, 1, 8, 9, 16, 24], np.int32), b.n)
+    for G in (None, 2, 8):
+        opt = sb.Options(force_group=G) if G else None
+        got = gpu_banded(sb, b, w, sb.BWA_MEM, sb.EXTEND, opt)
+        assert_same(got, oracle_banded(b, w, sb.BWA_MEM, oracle.EXTEND), b, w, f"left edge G={G}")
