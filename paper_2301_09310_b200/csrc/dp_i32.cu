@@ -39,9 +39,10 @@ __device__ __forceinline__ uint32_t prmt32(uint32_t a, uint32_t b, uint32_t c) {
 // runs FAST = false): the substitution is one PRMT from a per-row int8 table over the query codes,
 // sign-extended to 32 bits (query N / padding select the second source, a `mismatch` byte); the
 // EXTEND dead-zero rule is min(hdiag + s, lambda*hdiag) (one VIADDMNMX, lambda = 2^k >= match+1,
-// as in dp_i16.cu); and the per-row best is tracked per step on packed keys h*8 + (7 - x) (one
-// 3-input max per two cells, then one compare per row per step) instead of compare + 2 selects
-// per cell.  Same results: max h, first (smallest) column within the row.
+// as in dp_i16.cu); E is kept one column ahead and H = max3relu(D, E, F) (DPX, as dp_i16.cu); and
+// the per-row best is tracked per step on packed keys D*9 + (7 - x) (an IMAD, one 3-input max per
+// two cells, then one compare per row per step) instead of compare + 2 selects per cell.  Same
+// results: max value, first (smallest) column within the row.
 template <int G, int MODE, bool BAND, bool FAST>
 __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int bin) {
     const int lane = threadIdx.x & 31;
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
                 Hl[r] = MODE ? max(0, h0 - al - be * (r0 + r)) : 0;  // H(i,-1)
-                El[r] = 0;                                            // E(i,-1)
+                El[r] = FAST ? max(Hl[r] - al, -be) : 0;              // FAST: E(i,0); else E(i,-1)
                 bv[r] = MODE ? h0 : 0;                                // only cells beating this count
                 bc[r] = -1;
             }
@@ -161,7 +162,10 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                     for (int x = 0; x < 8; ++x) botH[x] = botF[x] = 0;
                     if (w >= 0 && w < blo) {  // left of my band: the column left of block blo is out of
 #pragma unroll                                 // band (H = E = 0), not the column -1 boundary
-                        for (int r = 0; r < 8; ++r) Hl[r] = El[r] = 0;
+                        for (int r = 0; r < 8; ++r) {
+                            Hl[r] = 0;
+                            El[r] = FAST ? -be : 0;  // FAST: E(i, 8*blo) = max(0 - alpha, 0 - beta)
+                        }
                     }
                     continue;
                 }
@@ -188,10 +192,12 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                         int hup = topH[x], fup = topF[x];
                         int hdiag = (x == 0) ? corner : topH[x - 1];
                         const int col = 8 * w + x;
+                        int haup = hup - al;  // FAST: H - alpha shared by the next row's F and my E
 #pragma unroll
                         for (int r = 0; r < 8; ++r) {
-                            const int e = max(Hl[r] - al, El[r] - be);
-                            const int f = max(hup - al, fup - be);
+                            // FAST keeps E one column ahead in El (as dp_i16.cu): e = E(i, j) here
+                            const int e = FAST ? El[r] : max(Hl[r] - al, El[r] - be);
+                            const int f = FAST ? __viaddmax_s32(fup, -be, haup) : max(hup - al, fup - be);
                             int d;
                             if constexpr (FAST) {
                                 const int sc = int(prmt32(tab[r], mmb, sel[x]));
@@ -200,11 +206,17 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                                 d = hdiag + ((tc[r] == qc[x]) ? ma : mm);
                                 if (MODE) d = (hdiag > 0) ? d : 0;
                             }
-                            int h = max(max(0, e), max(f, d));
+                            int h = FAST ? __vimax3_s32_relu(d, e, f) : max(max(0, e), max(f, d));
                             int ee = e, ff = f;
-                            if (BAND && edge && abs(r0 + r - col) > wb) h = ee = ff = 0;  // outside the band
+                            if (BAND && edge && abs(r0 + r - col) > wb) h = ee = ff = d = 0;  // outside the band
+                            const int ha = h - al;
+                            if constexpr (FAST) ee = __viaddmax_s32(ee, -be, ha);  // E(i, j+1)
                             if constexpr (FAST) {
-                                const int key = h * 8 + (7 - x);
+                                // keys over D, not H: the best cell is never a gap cell (a gap value is
+                                // below the cell it opened from), so the result is unchanged, and D
+                                // staying live keeps its add on the FMA pipe (as in dp_i16.cu); *9 is
+                                // an IMAD (FMA pipe) where *8 would be an ALU LEA
+                                const int key = d * 9 + (7 - x);
                                 if (x & 1) smax[r] = max(smax[r], max(kprev[r], key));
                                 else kprev[r] = key;
                             } else if (h > bv[r]) {
@@ -215,6 +227,7 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                             Hl[r] = h;
                             El[r] = ee;
                             hup = h;
+                            haup = ha;
                             fup = ff;
                         }
                         botH[x] = hup;
@@ -223,9 +236,9 @@ __global__ void __launch_bounds__(BLOCK_THREADS) dp_i32_kernel(AlignArgs a, int 
                     if constexpr (FAST) {
 #pragma unroll
                         for (int r = 0; r < 8; ++r)
-                            if ((smax[r] >> 3) > bv[r]) {
-                                bv[r] = smax[r] >> 3;
-                                bc[r] = 8 * w + 7 - (smax[r] & 7);
+                            if (smax[r] > bv[r] * 9 + 8) {  // key / 9 > bv
+                                bv[r] = smax[r] / 9;
+                                bc[r] = 8 * w + 7 - (smax[r] - 9 * bv[r]);
                             }
                     }
                     corner = topH[7];
