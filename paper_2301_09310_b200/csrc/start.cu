@@ -21,6 +21,18 @@
 
 namespace saloba {
 
+// bases of one packed word in reverse order (PACK4: byte swap + nibble swap; PACK2: bit reverse +
+// swap of the two bits of every field)
+template <int FMT>
+__device__ __forceinline__ uint32_t rev_bases(uint32_t x) {
+    if (FMT == SALOBA_PACK4) {
+        x = __byte_perm(x, 0, 0x0123);
+        return ((x >> 4) & 0x0F0F0F0Fu) | ((x & 0x0F0F0F0Fu) << 4);
+    }
+    x = __brev(x);
+    return ((x >> 1) & 0x55555555u) | ((x & 0x55555555u) << 1);
+}
+
 // One warp per pair (grid-stride).  Pairs whose forward score is <= 0 (no alignment, or an invalid
 // pair) get a 1-base prefix so the batch stays valid; their results are ignored by finalize.
 template <int FMT>
@@ -29,8 +41,6 @@ __global__ void reverse_prefix_kernel(const uint32_t* __restrict__ words, const 
                                       uint32_t* __restrict__ out, int32_t* __restrict__ out_len) {
     constexpr int B = FMT == SALOBA_PACK4 ? 8 : 16;      // bases per word
     constexpr int BITS = FMT == SALOBA_PACK4 ? 4 : 2;
-    constexpr uint32_t MASK = (1u << BITS) - 1u;
-    constexpr uint32_t PAD = FMT == SALOBA_PACK4 ? 15u : 0u;
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
     for (int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; p < n; p += warps) {
@@ -40,19 +50,14 @@ __global__ void reverse_prefix_kernel(const uint32_t* __restrict__ words, const 
         uint32_t* dst = out + word_off[p];
         const int nw = (len + B - 1) / B;
         for (int w = lane; w < nw; w += 32) {
-            const int hi = e - B * w;        // forward position of reversed base B*w (>= 0)
-            const int lo = hi - (B - 1);     // forward position of reversed base B*w + B - 1
-            const uint32_t whi = __ldg(src + hi / B);
-            const uint32_t wlo = (lo >= 0 && lo / B != hi / B) ? __ldg(src + lo / B) : whi;
-            uint32_t x = 0;
-#pragma unroll
-            for (int c = 0; c < B; ++c) {
-                const int fp = hi - c;
-                uint32_t code = PAD;
-                if (fp >= 0) code = (((fp / B) == (hi / B) ? whi : wlo) >> (BITS * (fp % B))) & MASK;
-                x |= code << (BITS * c);
-            }
-            dst[w] = x;
+            // reversed bases 8w.. (16w.. for PACK2) are forward positions hi, hi-1, ...: the
+            // concatenation [rev(word q-1) : rev(word q)] shifted so that position hi comes first
+            // (rev = base order reversed inside a word; word -1 = padding)
+            const int hi = e - B * w;
+            const int q = hi / B, o = hi % B;
+            const uint32_t wq = __ldg(src + q);
+            const uint32_t wp = q > 0 ? __ldg(src + q - 1) : (FMT == SALOBA_PACK4 ? 0xFFFFFFFFu : 0u);
+            dst[w] = __funnelshift_r(rev_bases<FMT>(wq), rev_bases<FMT>(wp), BITS * (B - 1 - o));
         }
         if (lane == 0) out_len[p] = len;
     }
