@@ -158,9 +158,17 @@ def cpu_baseline(batch, mode, seconds):
     import oracle  # the oracle, as it stands (cpu_baseline leg)
 
     r = oracle.timed_sample(batch, seconds=seconds, mode=mode)
+    r1 = oracle.timed_sample(batch, seconds=min(4.0, seconds / 3), mode=mode, threads=1)
+    model = ""
+    try:
+        model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+    except Exception:  # noqa: BLE001
+        pass
     return {"value": round(r["gcups"], 4), "unit": "GCUPS", "cores": r["threads"], "kind": "oracle",
+            "single_core_gcups": round(r1["gcups"], 4), "cpu_model": model, "nproc": os.cpu_count(),
             "sample": f"first {r['pairs']} pairs of the same workload ({r['cells']:.3e} cells, "
-                      f"{r['seconds']:.1f} s, full-matrix C oracle, {r['threads']} threads)"}
+                      f"{r['seconds']:.1f} s, full-matrix C oracle, {r['threads']} threads; single core "
+                      f"{r1['seconds']:.1f} s)"}
 
 
 def run_reference(args, world, rank):
@@ -275,16 +283,24 @@ def main():
     bins = torch.zeros(16, dtype=torch.int32, device=dev)
     long_group = torch.zeros(1, dtype=torch.int32, device=dev)
 
+    gather_events = []
+
     def step(dp_ev=None):
         o = sb.Options(args.force_group, args.force_path, args.keep_order, dp_ev, bins, args.i16_rows,
                        long_group) if dp_ev else None
         s, qe, te = al.run(qa, qo, ta, to, h0, options=o)
         if world > 1:  # A5: results gathered to rank 0 (the only collective; none inside the DP)
+            if dp_ev:
+                ge = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ge[0].record(stream)
+                gather_events.append(ge)
             send_buf[:, :n].copy_(al.out[:, :n])  # ranks own different counts: padded to the max
             if args.dist_backend == "nccl":
                 dist.gather(send_buf, gather_buf if rank == 0 else None, dst=0)
             else:  # gloo test hook: host copies
                 dist.gather(send_buf.cpu(), [g.cpu() for g in gather_buf] if rank == 0 else None, dst=0)
+            if dp_ev:
+                gather_events[-1][1].record(stream)
         return s
 
     for _ in range(args.warmup):
@@ -307,8 +323,10 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     for k in range(args.steps):
         step(dp_events[k])
+        step_ev[k].record(stream)
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -317,6 +335,8 @@ def main():
     clocks.stop()
     ms = ev0.elapsed_time(ev1)
     dp_ms = [a.elapsed_time(b) for a, b in dp_events]
+    step_ms = [ev0.elapsed_time(step_ev[0])] + [step_ev[k - 1].elapsed_time(step_ev[k]) for k in range(1, args.steps)]
+    gather_ms = sum(a.elapsed_time(b) for a, b in gather_events) / max(1, len(gather_events)) if gather_events else None
     t = torch.tensor([ms, sum(dp_ms) / len(dp_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         if args.dist_backend != "nccl":
@@ -469,6 +489,11 @@ def main():
         "metric": METRIC, "value": round(value, 2), "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": path, "data": "synthetic",
+        "step_ms": {"min": round(min(step_ms), 3), "median": round(float(np.median(step_ms)), 3),
+                    "max": round(max(step_ms), 3), "rank": 0},
+        "comms": None if gather_ms is None else {"gather_ms_per_step": round(gather_ms, 3),
+                                                  "share_of_step": round(gather_ms / ms_per_step, 4),
+                                                  "what": "NCCL gather of 12 B per pair to rank 0 (rank-0 stream)"},
         "config": {"workload": WORKLOADS[cfg], "mode": args.mode, "pairs_per_gpu": n,
                    "cells_per_step": total_cells, "scoring": "match 1, mismatch -4, alpha 7, beta 1 (BWA-MEM-style)",
                    "l2": "inputs larger than L2 (ASCII %.0f MB per GPU per step)" % ((len(batch.q_ascii) + len(batch.t_ascii)) / 1e6),
