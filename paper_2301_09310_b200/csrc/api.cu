@@ -246,9 +246,20 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
               ws + L.cub, L.cub_bytes};
     const int i16_rows = o.i16_rows == 8 ? 8 : I16_ROWS_DEFAULT;
     const int i32_fast = (sc.match <= 127 && sc.mismatch >= -128) ? 1 : 0;  // int8 substitution tables
+    // Latency floor for small batches: at G = 1 every int16x2 lane holds two pairs, so a batch of
+    // fewer pairs than resident lanes leaves most of the GPU idle and each pair takes its full
+    // single-lane latency; the smallest G with (n/2)*G >= resident lanes spreads the pairs instead
+    // (config 1, 1k pairs: the whole call becomes a few short chunks per pair).
+    int min_gidx = 0;
+    {
+        const int64_t lanes = int64_t(grid_for(d, int(mode), PATH_I16, 0, i16_rows)) * I16_THREADS;
+        const int64_t duos = (n_pairs + 1) / 2;
+        if (duos > 0 && duos * 2 < lanes)
+            while (min_gidx < NGROUPS - 1 && duos * (int64_t(1) << min_gidx) < lanes) ++min_gidx;
+    }
     ClassifyArgs ca{q_words, q_word_off, int(fmt), sc.match, q_len, t_len, h0, n_pairs, int(mode), force_g,
                     band_w ? 1 : o.force_path, o.keep_order, i16_rows, Qsup * 8, score, q_end, t_end, kv.keys_in,
-                    kv.vals_in, bin_count, (unsigned long long*)status, long_qmax, band_w, i32_fast};
+                    kv.vals_in, bin_count, (unsigned long long*)status, long_qmax, band_w, i32_fast, min_gidx};
     const int64_t cap16 = int64_t(grid_for(d, int(mode), PATH_I16, NGROUPS - 2, i16_rows)) * (I16_THREADS / 16) * 2;
     if (run_classify_sort(ca, kv, bin_start, d->sms, long_gidx, cap16, s) != cudaSuccess) return SALOBA_ECUDA;
 

@@ -78,6 +78,7 @@ struct ClassifyArgs {
     int32_t* long_qmax;  // max Q (8-base blocks) of the int16x2 long bin (atomicMax)
     const int32_t* band_w;  // NEXT-2: per-pair band half-width, or nullptr (banded pairs take the int32 path)
     int32_t i32_fast;       // 1: int32 pairs below the 2^28 value bound go to the FAST kernels (bins 0..5)
+    int32_t min_gidx;       // latency floor on log2(G) for batches too small to fill the GPU at G = 1
 };
 
 // Queries of >= LONG_Q blocks take the int16x2 "long bin" (bin PATH_I16*8 + NGROUPS-1); its width

@@ -120,13 +120,13 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
             // query N: the QN variant exists for G = 1 only (short reads, the common case)
             bool qn = false;
             if (elig == 2) {
-                qn = !a.band_w && choose_gidx(Q, m, a.force_gidx, 0, a.i16_rows, true) == 0;
+                qn = !a.band_w && choose_gidx(Q, m, a.force_gidx, a.min_gidx, a.i16_rows, true) == 0;
                 if (!qn) elig = 0;
             }
             const int path = elig ? PATH_I16 : PATH_I32;
-            int g = path == PATH_I16 ? choose_gidx(Q, m, a.force_gidx, 0, a.i16_rows, true)
+            int g = path == PATH_I16 ? choose_gidx(Q, m, a.force_gidx, a.min_gidx, a.i16_rows, true)
                     : a.band_w        ? choose_gidx_banded(Q, m, a.band_w[k], a.force_gidx)
-                                      : choose_gidx(Q, m, a.force_gidx, 1, I32_ROWS, false);  // int32 G=1 measured 3x slower than G=2
+                                      : choose_gidx(Q, m, a.force_gidx, max(1, a.min_gidx), I32_ROWS, false);  // int32 G=1 measured 3x slower than G=2
             if (path == PATH_I16 && a.force_gidx < 0 && g >= NGROUPS - 2) {
                 g = NGROUPS - 1;  // the long bin: G=16 or G=32 decided once it is counted
                 atomicMax(a.long_qmax, Q);
