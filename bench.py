@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--start-steps", type=int, default=3, help="LOCAL: time saloba_locate_start (0: skip)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="skip timing the step replayed from a CUDA graph (N=1 extra key cuda_graph)")
     ap.add_argument("--band", type=int, default=-1, help="NEXT-2: also time saloba_align_banded with this w")
     ap.add_argument("--band-steps", type=int, default=3)
     ap.add_argument("--partition", default="balanced", choices=["balanced", "equal"],
@@ -391,6 +393,31 @@ def main():
         e2e = {"value": round(e2e_val, 2), "unit": "GCUPS", "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": 12 * n * world, "api": "saloba_align_host_ctx (pinned host ASCII in, host results out, 4 pipelined slices of growing size)"}
 
+    # ---- optional: the same step captured once into a CUDA graph and replayed (launch-bound batches) ----
+    graph = None
+    if args.graph and world == 1:
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            al.run(qa, qo, ta, to, h0)  # warm on the capture stream
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=cap):
+                al.run(qa, qo, ta, to, h0)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        assert al.status.cpu().tolist()[:3] == [-1, -1, -1]
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            g.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = g0.elapsed_time(g1) / args.steps
+        graph = {"ms_per_step": round(gms, 4), "value": round(cells_rank / (gms * 1e-3) / 1e9, 2),
+                 "what": "pack + schedule + DP of one step captured once as a CUDA graph, replayed"}
+
     # ---- NEXT-3: start coordinates of the same LOCAL results (saloba_locate_start), timed alone ----
     start_pass = None
     if mode == sb.LOCAL and args.start_steps > 0:
@@ -501,7 +528,7 @@ def main():
                    "partition": partition_desc, "measured_rank_balance_max_over_mean": balance,
                    "gen_seconds": round(gen_s, 1)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-        "start_pass": start_pass, "banded": banded,
+        "start_pass": start_pass, "banded": banded, "cuda_graph": graph,
         "clocks": {"sm_mhz": csum["sm_mhz"], "sm_max_mhz": csum["sm_max_mhz"], "reasons": csum["reasons"]},
     }
     print(json.dumps(line), flush=True)
