@@ -99,3 +99,40 @@ def test_no_oracle_in_product_path():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "oracle" not in txt.lower().replace("oracle-independent", ""), f
+
+
+def test_host_checked_errors_new_entry_points(L):
+    """saloba_align_banded / saloba_locate_start / saloba_partition: argument errors are returned
+    synchronously, before any CUDA call (so they are checkable without a GPU)."""
+    import paper_2301_09310_b200 as sb
+
+    sc = sb.BWA_MEM._c()
+    nul = ctypes.c_void_p(0)
+    dummy = ctypes.c_void_p(256)
+    # banded: band array missing for n > 0
+    assert L.saloba_align_banded(dummy, dummy, dummy, dummy, dummy, dummy, nul, nul, 5, sc, 0, 4, dummy, dummy,
+                                 dummy, dummy, 1 << 20, dummy, None, nul) == sb.EINVAL
+    # start: null status, missing forward results, bad fmt, bad scheme, unaligned workspace
+    args = [dummy, dummy, 100, dummy, dummy, 100, 5, sc, 4, dummy, dummy, dummy, dummy, dummy, dummy, 1 << 20, dummy,
+            None, nul]
+    a = list(args); a[16] = nul
+    assert L.saloba_locate_start(*a) == sb.EINVAL
+    a = list(args); a[9] = nul
+    assert L.saloba_locate_start(*a) == sb.EINVAL
+    a = list(args); a[8] = 3
+    assert L.saloba_locate_start(*a) == sb.EINVAL
+    a = list(args); a[7] = sb.Scoring(1, -4, 1, 2)._c()
+    assert L.saloba_locate_start(*a) == sb.EINVAL
+    a = list(args); a[14] = ctypes.c_void_p(300)
+    assert L.saloba_locate_start(*a) == sb.EINVAL
+    a = list(args); a[15] = 16  # workspace smaller than the reversed-prefix buffers
+    assert L.saloba_locate_start(*a) == sb.EWORKSPACE
+    # partition: bad world, null workspace, too small workspace, negative n
+    assert L.saloba_partition_workspace_bytes(-1) == 0
+    need = L.saloba_partition_workspace_bytes(1000)
+    assert need >= 1000 * 24
+    assert L.saloba_partition(dummy, dummy, 1000, 0, dummy, dummy, need, nul) == sb.EINVAL
+    assert L.saloba_partition(dummy, dummy, 1000, 4, dummy, nul, need, nul) == sb.EINVAL
+    assert L.saloba_partition(dummy, dummy, 1000, 4, dummy, dummy, need - 1, nul) == sb.EWORKSPACE
+    assert L.saloba_partition(dummy, dummy, -1, 4, dummy, dummy, need, nul) == sb.EINVAL
+    assert L.saloba_partition(nul, nul, 0, 4, nul, dummy, need, nul) == sb.OK  # empty batch: nothing to do
