@@ -12,7 +12,7 @@ set -x
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/ablation
 python build_native.py > gpurun_out/ablation/build.log 2>&1 || { tail -30 gpurun_out/ablation/build.log; exit 1; }
-B="python bench.py --no-cpu-baseline --e2e-steps 0 --start-steps 0"
+B="python bench.py --no-cpu-baseline --e2e-steps 0 --start-steps 0 --no-graph"
 for g in 1 2 4 8 16 32; do
   timeout 300 $B --config 2 --pairs 300000 --steps 5 --force-group $g > gpurun_out/ablation/c2_i16_g$g.log 2>&1
   timeout 300 $B --config 2 --pairs 300000 --steps 3 --force-group $g --force-path 1 > gpurun_out/ablation/c2_i32_g$g.log 2>&1

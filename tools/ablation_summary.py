@@ -20,19 +20,24 @@ def bench(name):
 
 
 def ncu(path):
+    """Per-launch metrics of the full DP launches (>= half the longest); empty-bin launches exit
+    at once and are dropped.  Returns {metric: mean per big launch}, number of big launches."""
     rows = list(csv.DictReader(l for l in open(path) if l.startswith('"')))
-    agg = {}
-    launches = set()
+    per = {}
     for r in rows:
-        if not r.get("Kernel Name", "").startswith("void saloba::dp_i16_kernel") and "dp_i16_kernel" not in r.get("Kernel Name", ""):
+        if "dp_i16_kernel" not in r.get("Kernel Name", ""):
             continue
-        launches.add(r["ID"])
         v = float(r["Metric Value"].replace(",", "")) if r["Metric Value"] not in ("", "n/a") else 0.0
-        unit = r.get("Metric Unit", "")
         scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "nsecond": 1e-9, "usecond": 1e-6,
-                 "msecond": 1e-3}.get(unit, 1)
-        agg.setdefault(r["Metric Name"], []).append(v * scale)
-    return agg, len(launches)
+                 "msecond": 1e-3}.get(r.get("Metric Unit", ""), 1)
+        per.setdefault(r["ID"], {})[r["Metric Name"]] = v * scale
+    tmax = max((m.get("gpu__time_duration.sum", 0) for m in per.values()), default=0)
+    big = [m for m in per.values() if m.get("gpu__time_duration.sum", 0) >= 0.5 * tmax]  # the full DP launches
+    agg = {}
+    for m in big:
+        for k, v in m.items():
+            agg[k] = agg.get(k, 0.0) + v / len(big)
+    return agg, len(big)
 
 
 out = {"what": "On-B200 ablation (SURVEY §8(f) NEXT-4): subwarp size G, int16x2 vs int32 cells, scheduler on/off",
@@ -49,15 +54,15 @@ for p in sorted(glob.glob(os.path.join(A, "ncu_c2_g*.csv"))):
     agg, nl = ncu(p)
     if not agg:
         continue
-    dr = sum(agg.get("dram__bytes_read.sum", [0])) + sum(agg.get("dram__bytes_write.sum", [0]))
-    l2 = sum(agg.get("lts__t_bytes.sum", [0]))
-    alu = sum(agg.get("sm__inst_executed_pipe_alu.sum", [0]))
+    dr = agg.get("dram__bytes_read.sum", 0) + agg.get("dram__bytes_write.sum", 0)
+    l2 = agg.get("lts__t_bytes.sum", 0)
+    alu = agg.get("sm__inst_executed_pipe_alu.sum", 0)
     out["ncu_config2_100k"][f"G{g}"] = {
-        "launches": nl, "dram_bytes": dr, "dram_bytes_per_cell": round(dr / cells_100k, 4),
+        "dp_launches_with_work": nl, "dram_bytes_per_launch": dr, "dram_bytes_per_cell": round(dr / cells_100k, 4),
         "l2_bytes_per_cell": round(l2 / cells_100k, 4),
         "alu_warp_inst_per_cell": round(alu / cells_100k, 4),
-        "alu_pipe_pct": max(agg.get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", [0])),
-        "issue_active_pct": max(agg.get("smsp__issue_active.avg.pct_of_peak_sustained_active", [0])),
+        "alu_pipe_pct": round(agg.get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", 0), 1),
+        "issue_active_pct": round(agg.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0), 1),
         "model_spill_bytes_per_cell": round(8.0 / (16 * g), 4),
     }
 json.dump(out, open(os.path.join(ROOT, "profiles", "r01_ablation.json"), "w"), indent=1)
