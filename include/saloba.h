@@ -25,6 +25,11 @@
  * alpha ("gap_open") is the cost of a gap's FIRST base and beta ("gap_extend") of each further
  * base, literal to Eqs. 2-3 (BWA-MEM o=6,e=1 is alpha=7, beta=1).
  *
+ * Entry points: saloba_pack (A1); saloba_workspace_bytes + saloba_align_batch (A2-A4, device
+ * buffers); saloba_align_host[_ctx] (A1-A4 from host buffers); saloba_partition (A5, shards for
+ * the GPUs of one box); saloba_align_banded (banded DP);
+ * saloba_locate_start (LOCAL start coordinates, NEXT-3); diagnostics at the end.
+ *
  * Conventions for every entry point:
  *   - Pointers marked [dev] are device pointers owned by the caller (e.g. torch tensors); the
  *     library never frees them and allocates nothing on the hot path.  [host] are host pointers.
