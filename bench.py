@@ -396,14 +396,7 @@ def main():
     # ---- optional: the same step captured once into a CUDA graph and replayed (launch-bound batches) ----
     graph = None
     if args.graph and world == 1:
-        g = torch.cuda.CUDAGraph()
-        cap = torch.cuda.Stream()
-        cap.wait_stream(stream)
-        with torch.cuda.stream(cap):
-            al.run(qa, qo, ta, to, h0)  # warm on the capture stream
-            torch.cuda.synchronize()
-            with torch.cuda.graph(g, stream=cap):
-                al.run(qa, qo, ta, to, h0)
+        g = al.capture(qa, qo, ta, to, h0)
         torch.cuda.synchronize()
         g.replay()
         torch.cuda.synchronize()

@@ -50,14 +50,8 @@ def test_cuda_graph_replay_matches_stream_launch():
         ref = [x.clone() for x in al.run(qa, qo, ta, to, h0)]
         torch.cuda.synchronize()
         al.out.fill_(-7)
-        g = torch.cuda.CUDAGraph()
-        cap = torch.cuda.Stream()
-        cap.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(cap):
-            al.run(qa, qo, ta, to, h0)
-            torch.cuda.synchronize()
-            with torch.cuda.graph(g, stream=cap):
-                al.run(qa, qo, ta, to, h0)
+        g = al.capture(qa, qo, ta, to, h0)
+        torch.cuda.synchronize()
         al.out.fill_(-7)
         for _ in range(2):
             g.replay()
