@@ -479,7 +479,7 @@ def main():
     f_mhz = csum["sm_mhz"] or 1965.0
     bc = bins.cpu().tolist()
     lg = int(long_group.item())
-    n16, n32 = sum(bc[8:15]), sum(bc[0:8])  # bin 14 = int16x2 G=1 with N in the query
+    n16, n32 = sum(bc[8:15]) + bc[6], sum(bc[0:6]) + bc[7]  # bins 14 / 6: int16x2 G=1 / G=2 with N in the query
     path = "int16x2" if n16 >= n32 else "int32"
     opc = OPS_PER_CELL[(path, args.mode)]
     peak = sms * f_mhz * 1e6 * p_int / opc / 1e9
@@ -496,7 +496,7 @@ def main():
             "kernel": ("dp_i16_kernel" if path == "int16x2" else "dp_i32_kernel") +
                       " (all bins of one call, CUDA events on the launching stream)",
             # bin 13 = the int16x2 long bin, run at G = 2^long_group (16 or 32) this call
-            "bins": {("i16_G1_queryN" if b == 14 else
+            "bins": {("i16_G1_queryN" if b == 14 else "i16_G2_queryN" if b == 6 else
                       f"{'i16' if b >= 8 else 'i32'}_G{1 << (lg if b == 13 else b % 8)}{'_long' if b == 13 else ''}"): c
                      for b, c in enumerate(bc) if c and b != 15},
             "dp_share_of_step": round(dp_ms_avg / ms_per_step, 3),

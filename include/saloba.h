@@ -93,8 +93,9 @@ typedef struct {
                              path*8 + log2(G), path 0 = int32 exact, 1 = int16x2; bin 15 = invalid.
                              Bin 13 is the int16x2 "long bin" (queries >= 2048 bp and every pair the
                              cost model gives G >= 16): it runs at G=16 or G=32, see long_group.
-                             Bin 14: int16x2 G=1 pairs whose query contains N (an N column's
-                             substitution is forced to mismatch; other query-N pairs run int32) */
+                             Bins 14 / 6: int16x2 G=1 / G=2 pairs whose query contains N (an N
+                             column's substitution is forced to mismatch; other query-N pairs run
+                             int32).  Bin 7: int32 pairs whose values could reach 2^27 */
     int32_t* long_group;  /* optional [dev] int32[1]: log2(G) the long bin ran with this call (4 or 5):
                              G=16 iff the bin holds >= 4 waves of G=16 subwarps (throughput), else
                              G=32 (half the per-pair latency: few long pairs finish sooner) */

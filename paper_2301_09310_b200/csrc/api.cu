@@ -24,8 +24,8 @@ void launch_dp_i32(int mode, int gidx, int grid, const AlignArgs& a, int bin, cu
 const void* dp_i32_kernel_ptr(int mode, int gidx, bool band, bool fast);
 void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cudaStream_t s);
 const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt, int rows);
-const void* dp_i16_qn_kernel_ptr(int mode, int rows);
-void launch_dp_i16_qn(int mode, int grid, const AlignArgs& a, cudaStream_t s);
+const void* dp_i16_qn_kernel_ptr(int mode, int rows, int gidx);
+void launch_dp_i16_qn(int mode, int gidx, int grid, const AlignArgs& a, cudaStream_t s);
 void launch_reverse_prefix(int fmt, const uint32_t* words, const int64_t* word_off, const int32_t* end,
                            const int32_t* score, int64_t n, uint32_t* out, int32_t* out_len, int sms, cudaStream_t s);
 void launch_start_finalize(const int32_t* score, const int32_t* q_end, const int32_t* t_end, const int32_t* rscore,
@@ -41,7 +41,7 @@ struct DevInfo {
     int major = 0;
     int blocks_i32[2][NGROUPS] = {};
     int blocks_i16[2][2][NGROUPS] = {};  // [rows 8|16][mode][gidx]
-    int blocks_i16qn[2][2] = {};         // QN variant (G = 1): [rows 8|16][mode]
+    int blocks_i16qn[2][2][2] = {};      // QN variant: [rows 8|16][mode][G = 1|2]
     int max_blocks_per_sm = 1;           // max resident blocks of any DP kernel (block-slot pool)
     cudaStream_t aux[4] = {};            // bins run as concurrent kernels on these
 };
@@ -74,11 +74,11 @@ static const DevInfo* dev_info(int device) {
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i16_kernel_ptr(mode, g, SALOBA_PACK4, ri ? 16 : 8),
                                                                   I16_THREADS, 0);
                     d.blocks_i16[ri][mode][g] = std::max(1, nb);
-                    if (g == 0) {
+                    if (g <= 1) {
                         nb = 0;
-                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i16_qn_kernel_ptr(mode, ri ? 16 : 8),
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_i16_qn_kernel_ptr(mode, ri ? 16 : 8, g),
                                                                       I16_THREADS, 0);
-                        d.blocks_i16qn[ri][mode] = std::max(1, nb);
+                        d.blocks_i16qn[ri][mode][g] = std::max(1, nb);
                     }
                 }
             }
@@ -87,7 +87,8 @@ static const DevInfo* dev_info(int device) {
                 d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_i32[mode][g]);
                 for (int ri = 0; ri < 2; ++ri) {
                     d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_i16[ri][mode][g]);
-                    d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_i16qn[ri][mode]);
+                    d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_i16qn[ri][mode][0]);
+                    d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_i16qn[ri][mode][1]);
                 }
             }
         for (int i = 0; i < NAUX; ++i) cudaStreamCreateWithFlags(&d.aux[i], cudaStreamNonBlocking);
@@ -312,10 +313,12 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
             launch_dp_i32(int(mode), NGROUPS - 1, grid_for(d, int(mode), PATH_I32, NGROUPS - 1), a, I32_WIDE_BIN,
                           aux[(j + 1) % NAUX]);
         }
-        if (fmt == SALOBA_PACK4) {  // QN bin: int16x2 G=1 pairs whose query contains N
-            a.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(0), Qsup) + 8;
-            launch_dp_i16_qn(int(mode), d->sms * d->blocks_i16qn[i16_rows == 8 ? 0 : 1][int(mode)], a,
-                             aux[j % NAUX]);
+        if (fmt == SALOBA_PACK4) {  // QN bins: int16x2 G=1 / G=2 pairs whose query contains N
+            for (int g = 0; g <= 1; ++g) {
+                a.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(g), Qsup) + 8;
+                launch_dp_i16_qn(int(mode), g, d->sms * d->blocks_i16qn[i16_rows == 8 ? 0 : 1][int(mode)][g], a,
+                                 aux[(j + g) % NAUX]);
+            }
         }
         for (int i = 0; i < NAUX; ++i) {
             cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming);

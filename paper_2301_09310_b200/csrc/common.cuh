@@ -22,6 +22,7 @@ constexpr int BIN_SKIP = 15;
 // tables have no "never matches" slot for a query code).  Target N needs no fix-up: its rows use
 // an all-mismatch table.
 constexpr int QN_BIN = 14;
+constexpr int QN2_BIN = 6;  // the same variant at G = 2 (reads the cost model gives two lanes)
 // Bin 7: int32 pairs whose values could reach 2^28 (the packed best-cell keys of the FAST int32
 // kernel would overflow) or every int32 pair of a call whose scores do not fit int8; runs the plain
 // int32 kernel at G = 32.

@@ -638,16 +638,21 @@ static const void* kptr16_r(int mode, int gidx, int fmt) {
 const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt, int rows) {
     return rows == 8 ? kptr16_r<8>(mode, gidx, fmt) : kptr16_r<16>(mode, gidx, fmt);
 }
-// QN variant (query contains N): G = 1, PACK4 only (2-bit sequences cannot hold N)
-const void* dp_i16_qn_kernel_ptr(int mode, int rows) {
+// QN variant (query contains N): G = 1 (bin QN_BIN) or G = 2 (bin QN2_BIN), PACK4 only (2-bit
+// sequences cannot hold N)
+template <int G>
+static const void* kptr_qn(int mode, int rows) {
     if (rows == 8)
-        return mode == SALOBA_EXTEND ? (const void*)dp_i16_kernel<1, 8, 1, 4, true> : (const void*)dp_i16_kernel<1, 8, 0, 4, true>;
-    return mode == SALOBA_EXTEND ? (const void*)dp_i16_kernel<1, 16, 1, 4, true> : (const void*)dp_i16_kernel<1, 16, 0, 4, true>;
+        return mode == SALOBA_EXTEND ? (const void*)dp_i16_kernel<G, 8, 1, 4, true> : (const void*)dp_i16_kernel<G, 8, 0, 4, true>;
+    return mode == SALOBA_EXTEND ? (const void*)dp_i16_kernel<G, 16, 1, 4, true> : (const void*)dp_i16_kernel<G, 16, 0, 4, true>;
 }
-void launch_dp_i16_qn(int mode, int grid, const AlignArgs& a, cudaStream_t s) {
-    const void* fn = dp_i16_qn_kernel_ptr(mode, a.i16_rows);
+const void* dp_i16_qn_kernel_ptr(int mode, int rows, int gidx) {
+    return gidx == 0 ? kptr_qn<1>(mode, rows) : kptr_qn<2>(mode, rows);
+}
+void launch_dp_i16_qn(int mode, int gidx, int grid, const AlignArgs& a, cudaStream_t s) {
+    const void* fn = dp_i16_qn_kernel_ptr(mode, a.i16_rows, gidx);
     AlignArgs args = a;
-    int bin = QN_BIN;
+    int bin = gidx == 0 ? QN_BIN : QN2_BIN;
     void* params[] = {&args, &bin};
     cudaLaunchKernel(fn, dim3(grid), dim3(I16_THREADS), params, 0, s);
     count_launches(1);

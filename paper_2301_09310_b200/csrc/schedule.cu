@@ -117,10 +117,12 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
         } else {
             const int Q = (n + 7) >> 3;
             int elig = a.force_path != 1 ? i16_eligible(a, k, n, m) : 0;
-            // query N: the QN variant exists for G = 1 only (short reads, the common case)
+            // query N: the QN variant exists for G = 1 and G = 2 (short and mid-length reads)
             bool qn = false;
+            int qn_g = 0;
             if (elig == 2) {
-                qn = !a.band_w && choose_gidx(Q, m, a.force_gidx, a.min_gidx, a.i16_rows, true) == 0;
+                qn_g = choose_gidx(Q, m, a.force_gidx, a.min_gidx, a.i16_rows, true);
+                qn = !a.band_w && qn_g <= 1;
                 if (!qn) elig = 0;
             }
             const int path = elig ? PATH_I16 : PATH_I32;
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
                 g = NGROUPS - 1;  // the long bin: G=16 or G=32 decided once it is counted
                 atomicMax(a.long_qmax, Q);
             }
-            bin = qn ? QN_BIN : path * 8 + g;
+            bin = qn ? (qn_g == 0 ? QN_BIN : QN2_BIN) : path * 8 + g;
             if (path == PATH_I32) {
                 // FAST int32 kernels pack h*8 + column keys and form lambda*H: values must stay < 2^27
                 const long long mn = n < m ? n : m;

@@ -378,3 +378,20 @@ def test_small_batch_latency_floor(sb):
     bc = bins.cpu().tolist()
     assert bc[13] == b.n, bc
     assert_same(got, oracle_align(b, sb.BWA_MEM, 0), b, "small batch")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_query_n_bin_g2(sb, mode):
+    """Mid-length reads with N in the query (config 3 shapes) take the QN variant at G = 2 (bin 6)."""
+    import torch
+
+    b = synth.generate(3, 150_000, seed=43, p_n=0.002)
+    bins = torch.zeros(16, dtype=torch.int32, device="cuda")
+    got = gpu_align(sb, b, sb.BWA_MEM, mode, sb.Options(bin_counts=bins))
+    bc = bins.cpu().tolist()
+    assert bc[6] > 1000 and bc[14] > 1000, bc
+    rng = np.random.default_rng(43 + mode)
+    idx = np.sort(rng.choice(b.n, 4000, replace=False))
+    idx = np.unique(np.concatenate([idx, np.nonzero(b.qlen > 640)[0][:500]]))
+    sub = b.subset(idx)
+    assert_same(tuple(x[idx] for x in got[:3]), oracle_align(sub, sb.BWA_MEM, mode), sub, f"QN G=2 mode={mode}")
