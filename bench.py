@@ -70,6 +70,11 @@ def parse():
     ap.add_argument("--i16-rows", type=int, default=0)
     ap.add_argument("--p-n", type=float, default=0.0, help="probability of N per base (real reads carry a few)")
     ap.add_argument("--grouped", action="store_true", help="config 5: components contiguous")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the global batch is --pairs (default: the config's count) pairs "
+                         "whatever N; default is weak scaling (N x pairs)")
+    ap.add_argument("--dump-results", default=None,
+                    help="rank 0 saves the (3, n_total) results of the last timed step, input order (.npy)")
     ap.add_argument("--dist-backend", default="nccl", help="test hook: gloo lets several ranks share one GPU")
     return ap.parse_args()
 
@@ -240,33 +245,41 @@ def main():
         return t.numpy()[:nbytes]
 
     t0 = time.time()
-    n_total = world * n
+    # weak scaling (default): every rank owns `n` pairs of a world*n-pair global batch; strong
+    # scaling (--strong): the global batch is `n` pairs whatever the world size
+    n_total = n if args.strong else world * n
     partition_desc = "single GPU"
+    from paper_2301_09310_b200 import dist as sd
+
     if world > 1 and args.partition == "balanced":
         # A5: every rank computes the same length-balanced partition of the global
         # batch on its own GPU (saloba_partition: cost sort + snake deal; deterministic, so no
         # collective) and generates only the pairs it owns.
-        from paper_2301_09310_b200 import dist as sd
-
         gql, gtl, _ = synth.shapes(cfg, n_total, seed=cfg, grouped=args.grouped)
         owner = sd.balanced_partition(gql, gtl, world)
-        mine = np.nonzero(owner == rank)[0]
+        index_of_rank = [np.nonzero(owner == r)[0] for r in range(world)]
         cost = sd.pair_cost(gql, gtl)
         partition_desc = f"length-balanced snake over {world} ranks (saloba_partition), modelled max/mean {sd.imbalance(cost, owner, world):.4f}"
-        total_cells_global = int(np.dot(gql.astype(np.int64), gtl.astype(np.int64)))
-        counts = np.bincount(owner, minlength=world).tolist()
-        batch = synth.generate_idx(cfg, mine, n_total, seed=cfg, grouped=args.grouped, p_n=args.p_n, out=alloc)
+        batch = synth.generate_idx(cfg, index_of_rank[rank], n_total, seed=cfg, grouped=args.grouped, p_n=args.p_n,
+                                   out=alloc)
         del gql, gtl, owner, cost
     else:
         if world > 1:
             partition_desc = f"equal contiguous split over {world} ranks"
-        batch = synth.generate(cfg, n, seed=cfg, first=rank * n, n_total=n_total, grouped=args.grouped, p_n=args.p_n,
+        ranges = [sd.shard_range(n_total, world, r) for r in range(world)]
+        index_of_rank = [np.arange(a_, b_) for a_, b_ in ranges]
+        a_, b_ = ranges[rank]
+        batch = synth.generate(cfg, b_ - a_, seed=cfg, first=a_, n_total=n_total, grouped=args.grouped, p_n=args.p_n,
                                out=alloc)
-        counts = [n] * world
-        total_cells_global = None
+    counts = [len(ix) for ix in index_of_rank]
     n = batch.n  # pairs on this rank
     gen_s = time.time() - t0
     cells_rank = batch.cells()
+    total_cells = cells_rank
+    if world > 1:
+        tc = torch.tensor([cells_rank], dtype=torch.int64, device=dev if args.dist_backend == "nccl" else "cpu")
+        dist.all_reduce(tc)
+        total_cells = int(tc[0])
     max_q = int(batch.qlen.max())
     qa = torch.from_numpy(batch.q_ascii).to(dev)
     ta = torch.from_numpy(batch.t_ascii).to(dev)
@@ -279,13 +292,24 @@ def main():
     gather_buf = None
     nmax = max(counts)
     send_buf = torch.full((3, nmax), -9, dtype=torch.int32, device=dev) if world > 1 else None
-    if world > 1:
-        gather_buf = [torch.empty((3, nmax), dtype=torch.int32, device=dev) for _ in range(world)] if rank == 0 else None
+    full_out = full_status = index_dev = None
+    if world > 1 and rank == 0:
+        # A5 reassembly on rank 0: the gathered shards (world, 3, nmax) go back to input order by
+        # saloba_scatter_results, with each column's global index (-1 = padding)
+        gathered = torch.empty((world, 3, nmax), dtype=torch.int32, device=dev)
+        gather_buf = list(gathered.unbind(0))
+        idx_host = np.full((world, nmax), -1, np.int32)
+        for r, ix in enumerate(index_of_rank):
+            idx_host[r, :len(ix)] = ix
+        index_dev = torch.from_numpy(idx_host).to(dev)
+        full_out = torch.full((3, n_total), -9, dtype=torch.int32, device=dev)
 
     bins = torch.zeros(16, dtype=torch.int32, device=dev)
     long_group = torch.zeros(1, dtype=torch.int32, device=dev)
 
     gather_events = []
+
+    full_status = None
 
     def step(dp_ev=None):
         o = sb.Options(args.force_group, args.force_path, args.keep_order, dp_ev, bins, args.i16_rows,
@@ -300,7 +324,13 @@ def main():
             if args.dist_backend == "nccl":
                 dist.gather(send_buf, gather_buf if rank == 0 else None, dst=0)
             else:  # gloo test hook: host copies
-                dist.gather(send_buf.cpu(), [g.cpu() for g in gather_buf] if rank == 0 else None, dst=0)
+                host = [torch.empty((3, nmax), dtype=torch.int32) for _ in range(world)] if rank == 0 else None
+                dist.gather(send_buf.cpu(), host, dst=0)
+                if rank == 0:
+                    gathered.copy_(torch.stack(host))
+            if rank == 0:
+                nonlocal full_status
+                _, full_status = sb.scatter_results(gathered, index_dev, n_total, out=full_out)
             if dp_ev:
                 gather_events[-1][1].record(stream)
         return s
@@ -310,6 +340,8 @@ def main():
     torch.cuda.synchronize()
     st = al.status.cpu().tolist()
     assert st[0] == -1 and st[1] == -1 and st[2] == -1, f"bad status {st}"
+    if full_status is not None:
+        assert int(full_status.item()) == -1 and int((full_out == -9).sum().item()) == 0, "reassembly incomplete"
 
     dp_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                  for _ in range(args.steps)]
@@ -339,6 +371,9 @@ def main():
     dp_ms = [a.elapsed_time(b) for a, b in dp_events]
     step_ms = [ev0.elapsed_time(step_ev[0])] + [step_ev[k - 1].elapsed_time(step_ev[k]) for k in range(1, args.steps)]
     gather_ms = sum(a.elapsed_time(b) for a, b in gather_events) / max(1, len(gather_events)) if gather_events else None
+    if args.dump_results and rank == 0:  # the reassembled results of the last timed step, input order
+        res = full_out if world > 1 else al.out[:, :n]
+        np.save(args.dump_results, res.cpu().numpy())
     t = torch.tensor([ms, sum(dp_ms) / len(dp_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         if args.dist_backend != "nccl":
@@ -346,7 +381,6 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, dp_ms_avg = float(t[0]), float(t[1])
     ms_per_step = ms_max / args.steps
-    total_cells = total_cells_global if total_cells_global is not None else cells_rank * world
     # per-rank balance of the measured step time (max/mean over ranks)
     balance = None
     if world > 1:
@@ -507,17 +541,18 @@ def main():
         cpu = cpu_baseline(batch, mode, args.cpu_seconds)
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": path, "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": path, "data": "synthetic",
         "step_ms": {"min": round(min(step_ms), 3), "median": round(float(np.median(step_ms)), 3),
                     "max": round(max(step_ms), 3), "rank": 0},
         "comms": None if gather_ms is None else {"gather_ms_per_step": round(gather_ms, 3),
                                                   "share_of_step": round(gather_ms / ms_per_step, 4),
-                                                  "what": "NCCL gather of 12 B per pair to rank 0 (rank-0 stream)"},
+                                                  "what": "NCCL gather of 12 B per pair to rank 0 + saloba_scatter_results back to input order (rank-0 stream)"},
         "config": {"workload": WORKLOADS[cfg], "mode": args.mode, "pairs_per_gpu": n,
                    "cells_per_step": total_cells, "scoring": "match 1, mismatch -4, alpha 7, beta 1 (BWA-MEM-style)",
                    "l2": "inputs larger than L2 (ASCII %.0f MB per GPU per step)" % ((len(batch.q_ascii) + len(batch.t_ascii)) / 1e6),
-                   "parallelism": f"pairs sharded over {world} GPU(s), results gathered to rank 0",
+                   "parallelism": f"pairs sharded over {world} GPU(s), results gathered to rank 0 and put back in input order",
+                   "pairs_total": n_total,
                    "partition": partition_desc, "measured_rank_balance_max_over_mean": balance,
                    "gen_seconds": round(gen_s, 1)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

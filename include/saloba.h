@@ -28,7 +28,8 @@
  * Entry points: saloba_pack (A1); saloba_workspace_bytes + saloba_align_batch (A2-A4, device
  * buffers); saloba_align_host[_ctx] (A1-A4 from host buffers); saloba_partition (A5, shards for
  * the GPUs of one box); saloba_align_banded (banded DP);
- * saloba_locate_start (LOCAL start coordinates, NEXT-3); diagnostics at the end.
+ * saloba_locate_start (LOCAL start coordinates, NEXT-3); saloba_scatter_results (A5, rank 0
+ * puts gathered shards back in input order); diagnostics at the end.
  *
  * Conventions for every entry point:
  *   - Pointers marked [dev] are device pointers owned by the caller (e.g. torch tensors); the
@@ -222,6 +223,22 @@ size_t saloba_partition_workspace_bytes(int64_t n_pairs);
  * Asynchronous on `stream`.  Host-checked errors only (EINVAL / EWORKSPACE). */
 int saloba_partition(const int32_t* q_len, const int32_t* t_len, int64_t n_pairs, int32_t world, int32_t* owner,
                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* Rank 0's reassembly step (SURVEY §8(e) "rank 0 unpermutes with the partition it computed"):
+ * the shards gathered from `world` ranks are written back to input order.
+ *   parts    [dev] int32[world][3][stride]   rank r's results (rows score, q_end, t_end), as
+ *                                            gathered (each shard padded to `stride` columns)
+ *   index    [dev] int32[world][stride]      global input index of each gathered column; -1 marks
+ *                                            a padding column (ignored)
+ *   score, q_end, t_end  [dev] int32[n_total]  output, input order
+ *   status   [dev] int64[1]   -1, or the smallest flat slot r*stride+i whose index is >= n_total
+ *                             (inconsistent index; that column is not written)
+ * Every index in 0..n_total-1 should appear exactly once; positions no rank owns are left as they
+ * were.  Asynchronous on `stream`.  Host-checked: pointers, stride >= 0, world >= 1,
+ * 0 <= n_total <= INT32_MAX. */
+int saloba_scatter_results(const int32_t* parts, const int32_t* index, int64_t stride, int32_t world,
+                           int64_t n_total, int32_t* score, int32_t* q_end, int32_t* t_end, int64_t* status,
+                           void* stream);
 
 /* ---- end-to-end from host buffers ----------------------------------------------------------- */
 

@@ -15,7 +15,7 @@ import torch
 
 __all__ = [
     "LOCAL", "EXTEND", "PACK4", "PACK2", "Scoring", "Options", "BWA_MEM", "SalobaError", "lib", "lib_path",
-    "packed_words", "pack", "workspace_bytes", "align_batch", "align", "align_banded", "start_workspace_bytes", "locate_start", "partition",
+    "packed_words", "pack", "workspace_bytes", "align_batch", "align", "align_banded", "start_workspace_bytes", "locate_start", "partition", "scatter_results",
     "align_host", "version", "EXPORTS",
 ]
 
@@ -26,7 +26,7 @@ OK, EINVAL, ECUDA, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4
 #: every symbol include/saloba.h declares
 EXPORTS = ("saloba_packed_words", "saloba_pack", "saloba_workspace_bytes", "saloba_align_batch",
            "saloba_align_banded", "saloba_start_workspace_bytes", "saloba_locate_start",
-           "saloba_partition_workspace_bytes", "saloba_partition",
+           "saloba_partition_workspace_bytes", "saloba_partition", "saloba_scatter_results",
            "saloba_host_ctx_create", "saloba_host_ctx_destroy", "saloba_align_host_ctx", "saloba_align_host",
            "saloba_strerror", "saloba_version", "saloba_kernel_launches")
 
@@ -119,6 +119,8 @@ def lib() -> ctypes.CDLL:
         L.saloba_partition_workspace_bytes.restype = ctypes.c_size_t
         L.saloba_partition.argtypes = [vp, vp, i64, i32, vp, vp, ctypes.c_size_t, vp]
         L.saloba_partition.restype = ctypes.c_int
+        L.saloba_scatter_results.argtypes = [vp, vp, i64, i32, i64, vp, vp, vp, vp, vp]
+        L.saloba_scatter_results.restype = ctypes.c_int
         L.saloba_start_workspace_bytes.argtypes = [i64, i64, i64, i32, ctypes.c_int]
         L.saloba_start_workspace_bytes.restype = ctypes.c_size_t
         L.saloba_locate_start.argtypes = [vp, vp, i64, vp, vp, i64, i64, _Scoring, ctypes.c_int, vp, vp, vp, vp, vp,
@@ -278,6 +280,23 @@ def partition(q_len: torch.Tensor, t_len: torch.Tensor, world: int, stream=None)
     _check(lib().saloba_partition(_p(q_len), _p(t_len), n, world, _p(owner), _p(ws), ws.numel(), _stream(stream)),
            "saloba_partition")
     return owner[:n]
+
+
+def scatter_results(parts: torch.Tensor, index: torch.Tensor, n_total: int, out: torch.Tensor | None = None,
+                    stream=None):
+    """A5 reassembly (saloba_scatter_results): parts (world, 3, stride) int32 as gathered, index
+    (world, stride) int32 global input index per column (-1 = padding) -> (out (3, n_total), status)."""
+    parts = _dev_tensor(parts, torch.int32, "parts")
+    index = _dev_tensor(index, torch.int32, "index")
+    if parts.dim() != 3 or parts.shape[1] != 3 or index.shape != (parts.shape[0], parts.shape[2]):
+        raise ValueError("parts must be (world, 3, stride) and index (world, stride)")
+    world, stride = int(index.shape[0]), int(index.shape[1])
+    if out is None:
+        out = torch.full((3, max(n_total, 1)), -9, dtype=torch.int32, device=parts.device)
+    status = torch.empty(1, dtype=torch.int64, device=parts.device)
+    _check(lib().saloba_scatter_results(_p(parts), _p(index), stride, world, n_total, _p(out[0]), _p(out[1]),
+                                        _p(out[2]), _p(status), _stream(stream)), "saloba_scatter_results")
+    return out, status
 
 
 def start_workspace_bytes(n_pairs: int, q_words_total: int, t_words_total: int, max_qlen: int,

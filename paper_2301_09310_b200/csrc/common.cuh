@@ -11,6 +11,11 @@ namespace saloba {
 
 // process-wide count of this library's own kernel launches (saloba_kernel_launches)
 void count_launches(int n);
+// SM count of the current device (cached per device, api.cu)
+int sm_count_current();
+// status word helpers (pack.cu): init to "no error" (all ones), final maps it to -1 / first index
+void launch_status_init(int64_t* st, cudaStream_t s);
+void launch_status_final(int64_t* st, cudaStream_t s);
 
 // ---- bins ------------------------------------------------------------------------------------
 // bin = path * 8 + gidx; gidx = log2(G) (G in {1,2,4,8,16,32}); path 0 = int32 exact kernel,

@@ -67,11 +67,56 @@ SALOBA_API int saloba_partition(const int32_t* q_len, const int32_t* t_len, int6
     void* tmp = ws + 2 * al256(nn * 8) + 2 * al256(nn * 4);
     size_t tb = sort_bytes(n_pairs);
     const int64_t need = (n_pairs + 255) / 256;
-    const int grid = int(need < 148 * 8 ? need : 148 * 8);
+    const int64_t cap = int64_t(sm_count_current()) * 8;
+    const int grid = int(need < cap ? need : cap);
     partition_cost_kernel<<<grid, 256, 0, s>>>(q_len, t_len, n_pairs, kin, vin);
     if (cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, int(n_pairs), 0, 64, s) != cudaSuccess)
         return SALOBA_ECUDA;
     partition_snake_kernel<<<grid, 256, 0, s>>>(vout, n_pairs, world, owner);
     count_launches(2);
+    return cudaGetLastError() == cudaSuccess ? SALOBA_OK : SALOBA_ECUDA;
+}
+
+// ---- A5 reassembly: gathered per-rank results back to input order ("Rank 0
+// unpermutes with the partition it computed") ------------------------------------------------------
+namespace saloba {
+__global__ void scatter_results_kernel(const int32_t* __restrict__ parts, const int32_t* __restrict__ index,
+                                       int64_t stride, int64_t world_stride, int64_t n_total,
+                                       int32_t* __restrict__ score, int32_t* __restrict__ q_end,
+                                       int32_t* __restrict__ t_end, unsigned long long* __restrict__ status) {
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < world_stride;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t dst = index[k];
+        if (dst < 0) continue;  // padding slot of a shorter shard
+        if (int64_t(dst) >= n_total) {
+            atomicMin(status, (unsigned long long)k);
+            continue;
+        }
+        const int64_t r = k / stride, i = k - r * stride;
+        const int32_t* p = parts + r * 3 * stride;  // rank r's (3, stride) block: score, q_end, t_end rows
+        score[dst] = p[i];
+        q_end[dst] = p[stride + i];
+        t_end[dst] = p[2 * stride + i];
+    }
+}
+}  // namespace saloba
+
+SALOBA_API int saloba_scatter_results(const int32_t* parts, const int32_t* index, int64_t stride, int32_t world,
+                                      int64_t n_total, int32_t* score, int32_t* q_end, int32_t* t_end,
+                                      int64_t* status, void* stream) {
+    if (stride < 0 || world < 1 || n_total < 0 || n_total > int64_t(INT32_MAX) || !status) return SALOBA_EINVAL;
+    if (stride > 0 && (!parts || !index)) return SALOBA_EINVAL;
+    if (n_total > 0 && (!score || !q_end || !t_end)) return SALOBA_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    launch_status_init(status, s);
+    const int64_t total = stride * int64_t(world);
+    if (total > 0) {
+        const int64_t need = (total + 255) / 256;
+        const int cap = sm_count_current() * 8;
+        scatter_results_kernel<<<int(need < cap ? need : cap), 256, 0, s>>>(
+            parts, index, stride, total, n_total, score, q_end, t_end, (unsigned long long*)status);
+        count_launches(1);
+    }
+    launch_status_final(status, s);
     return cudaGetLastError() == cudaSuccess ? SALOBA_OK : SALOBA_ECUDA;
 }

@@ -74,6 +74,9 @@ __host__ __device__ inline int choose_gidx_banded(int Q, int m, int w, int force
 }
 
 __device__ inline int i16_eligible(const ClassifyArgs& a, int64_t k, int n, int m) {  // 0: int32, 1: int16x2, 2: int16x2 with N in the query (QN)
+    // the int16x2 kernels build their substitution rows as int8 bytes (dp_i16.cu row_table, PRMT
+    // sign replication): a call whose match or mismatch does not fit int8 is int32-only
+    if (!a.i32_fast) return 0;
     const long long mn = n < m ? n : m;
     long long B = (long long)a.match * mn;
     long long lam = 1;

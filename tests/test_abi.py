@@ -136,3 +136,18 @@ def test_host_checked_errors_new_entry_points(L):
     assert L.saloba_partition(dummy, dummy, 1000, 4, dummy, dummy, need - 1, nul) == sb.EWORKSPACE
     assert L.saloba_partition(dummy, dummy, -1, 4, dummy, dummy, need, nul) == sb.EINVAL
     assert L.saloba_partition(nul, nul, 0, 4, nul, dummy, need, nul) == sb.OK  # empty batch: nothing to do
+
+
+def test_host_checked_errors_scatter_results(L):
+    """saloba_scatter_results (A5 reassembly): argument errors are returned before any CUDA call."""
+    import paper_2301_09310_b200 as sb
+
+    nul = ctypes.c_void_p(0)
+    dummy = ctypes.c_void_p(256)
+    assert L.saloba_scatter_results(dummy, dummy, 10, 2, 20, dummy, dummy, dummy, nul, nul) == sb.EINVAL  # no status
+    assert L.saloba_scatter_results(nul, dummy, 10, 2, 20, dummy, dummy, dummy, dummy, nul) == sb.EINVAL  # no parts
+    assert L.saloba_scatter_results(dummy, nul, 10, 2, 20, dummy, dummy, dummy, dummy, nul) == sb.EINVAL  # no index
+    assert L.saloba_scatter_results(dummy, dummy, 10, 0, 20, dummy, dummy, dummy, dummy, nul) == sb.EINVAL  # world 0
+    assert L.saloba_scatter_results(dummy, dummy, -1, 2, 20, dummy, dummy, dummy, dummy, nul) == sb.EINVAL
+    assert L.saloba_scatter_results(dummy, dummy, 10, 2, 20, nul, dummy, dummy, dummy, nul) == sb.EINVAL  # no output
+    assert L.saloba_scatter_results(dummy, dummy, 10, 2, 1 << 31, dummy, dummy, dummy, dummy, nul) == sb.EINVAL
