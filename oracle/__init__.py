@@ -40,6 +40,10 @@ def _lib():
         lib.oracle_banded_batch.argtypes = [p, p, p, p, p, p, i64, i32, i32, i32, i32, i, p, p, p, p, i]
         lib.oracle_start.argtypes = [p, i, p, i, i32, i32, i32, i32, p]
         lib.oracle_start_batch.argtypes = [p, p, p, p, i64, i32, i32, i32, i32, p, p, p, p, p, p, i]
+        ksw = [p, i, p, i] + [i32] * 11 + [p]
+        lib.oracle_ksw_extend.argtypes = ksw
+        lib.oracle_ksw_table.argtypes = ksw + [p]
+        lib.oracle_ksw_batch.argtypes = [p, p, p, p, p, i64, p, i32, p, p, i]
         _LIB = lib
     return _LIB
 
@@ -183,3 +187,52 @@ def timed_sample(batch, seconds=10.0, mode=LOCAL, threads=None, **sc):
             k *= 2
     return dict(gcups=cells_tot / t_tot / 1e9 if t_tot > 0 else 0.0, cells=cells_tot, pairs=pairs_tot,
                 seconds=t_tot, threads=threads)
+
+
+# ---- BWA-MEM-compatible extension (oracle/ksw.c, reading 17) ----
+KSW_NO_TRIM = 1
+#: BWA-MEM defaults: a=1, b=4, o_del=e_del... (o=6, e=1), band w=100, end_bonus=5, zdrop=100
+KSW_BWA = dict(a=1, b=4, o_del=6, e_del=1, o_ins=6, e_ins=1, w=100, end_bonus=5, zdrop=100)
+KSW_FIELDS = ("score", "qle", "tle", "gtle", "gscore", "max_off", "clip")
+
+
+def _ksw_params(kw):
+    p = dict(KSW_BWA)
+    p.update(kw)
+    return [p[k] for k in ("a", "b", "o_del", "e_del", "o_ins", "e_ins", "w", "end_bonus", "zdrop")]
+
+
+def ksw_extend(q, t, h0, flags=0, table=False, **kw):
+    """BWA-MEM ksw_extend2 of one pair: dict of KSW_FIELDS (+ 'H': m x n table, -1 = not computed,
+    when table=True).  Raises ValueError with the oracle status on invalid input."""
+    q, t = _b(q), _b(t)
+    out = (ctypes.c_int32 * 7)()
+    args = [_buf(q), len(q), _buf(t), len(t), *_ksw_params(kw), h0, flags, out]
+    if table:
+        H = np.full((max(len(t), 1), max(len(q), 1)), -1, np.int32)
+        st = _lib().oracle_ksw_table(*args, H.ctypes.data)
+    else:
+        st = _lib().oracle_ksw_extend(*args)
+    if st != OK:
+        raise ValueError(st)
+    r = dict(zip(KSW_FIELDS, (int(x) for x in out)))
+    if table:
+        r["H"] = H
+    return r
+
+
+def ksw_batch(batch, flags=0, threads=None, **kw):
+    """ksw_extend2 over a synth.Batch-like object: (out int32[7, n] rows = KSW_FIELDS, status int32[n])."""
+    n = len(batch.q_off) - 1
+    out = np.empty((7, max(n, 1)), np.int32)
+    st = np.empty(max(n, 1), np.int32)
+    threads = threads or os.cpu_count() or 1
+    qa = np.ascontiguousarray(batch.q_ascii)
+    ta = np.ascontiguousarray(batch.t_ascii)
+    qo = np.ascontiguousarray(batch.q_off, np.int64)
+    to = np.ascontiguousarray(batch.t_off, np.int64)
+    h0 = np.ascontiguousarray(batch.h0, np.int32)
+    par = np.array(_ksw_params(kw), np.int32)
+    _lib().oracle_ksw_batch(qa.ctypes.data, qo.ctypes.data, ta.ctypes.data, to.ctypes.data, h0.ctypes.data, n,
+                            par.ctypes.data, flags, out.ctypes.data, st.ctypes.data, threads)
+    return out[:, :n], st[:n]
