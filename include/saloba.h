@@ -29,7 +29,8 @@
  * buffers); saloba_align_host[_ctx] (A1-A4 from host buffers); saloba_partition (A5, shards for
  * the GPUs of one box); saloba_align_banded (banded DP);
  * saloba_locate_start (LOCAL start coordinates, NEXT-3); saloba_scatter_results (A5, rank 0
- * puts gathered shards back in input order); diagnostics at the end.
+ * puts gathered shards back in input order); saloba_ksw_extend (BWA-MEM-compatible extension,
+ * NEXT-1); diagnostics at the end.
  *
  * Conventions for every entry point:
  *   - Pointers marked [dev] are device pointers owned by the caller (e.g. torch tensors); the
@@ -239,6 +240,45 @@ int saloba_partition(const int32_t* q_len, const int32_t* t_len, int64_t n_pairs
 int saloba_scatter_results(const int32_t* parts, const int32_t* index, int64_t stride, int32_t world,
                            int64_t n_total, int32_t* score, int32_t* q_end, int32_t* t_end, int64_t* status,
                            void* stream);
+
+/* ---- BWA-MEM-compatible seed extension ------------------------------------ */
+
+/* BWA-MEM's extension parameters (mem_opt_t): scores a (match), b (mismatch penalty, > 0), N
+ * scores -1; a deletion of k target bases costs o_del + k*e_del, an insertion of k query bases
+ * o_ins + k*e_ins; band w; end_bonus; zdrop (0 disables).  BWA-MEM defaults: a 1, b 4, o 6, e 1,
+ * w 100, end_bonus 5, zdrop 100. */
+typedef struct {
+    int32_t a, b, o_del, e_del, o_ins, e_ins, w, end_bonus, zdrop;
+} saloba_ksw_params;
+
+/* Workspace (bytes) for saloba_ksw_extend on n_pairs pairs whose queries are <= max_qlen bases
+ * (0 on a bad argument or device). */
+size_t saloba_ksw_workspace_bytes(int64_t n_pairs, int32_t max_qlen, int device);
+
+/* Seed extension with BWA-MEM's ksw_extend2 semantics (PAPER.md P:1300-1306 — the paper's real
+ * inputs are BWA-MEM seeds; the definition is DESIGN.md reading 17): gaps open from
+ * the match state only, separate insertion / deletion costs, N scores -1, the band w (lowered by
+ * BWA's max_ins / max_del bounds), per-row trimming to the previous row's nonzero extent + 2,
+ * z-drop, the end-to-end score of the last query column, BWA's tie rules (first row, LAST column).
+ *   q_words..t_len, fmt  [dev] packed pairs as for saloba_align_batch
+ *   h0                   [dev] int32[n_pairs] seed scores, 1 .. 2^29
+ *   params               [host] see saloba_ksw_params (|values| <= 2^10, w >= 0, zdrop >= 0)
+ *   max_qlen             the longest query (sizes the per-warp row buffers; longer queries are
+ *                        reported as invalid)
+ *   out                  [dev] int32[7][n_pairs], rows: score (max), qle, tle (ends, exclusive;
+ *                        0 when nothing beats h0), gtle, gscore (end-to-end score at the last query
+ *                        column, -1 if no row reached it), max_off, clip (1: BWA-MEM keeps the
+ *                        local extension, 0: it takes the end-to-end one: gscore > 0 and
+ *                        gscore > score - end_bonus)
+ *   status               [dev] int64[1]: -1 or the smallest invalid pair (length 0 or > 2^20, h0
+ *                        out of range, query longer than max_qlen, values that could overflow
+ *                        int32); such pairs get score -1 and -2 elsewhere
+ * Asynchronous on `stream`; host-checked errors as
+ * saloba_align_batch. */
+int saloba_ksw_extend(const uint32_t* q_words, const int64_t* q_word_off, const int32_t* q_len,
+                      const uint32_t* t_words, const int64_t* t_word_off, const int32_t* t_len, const int32_t* h0,
+                      int64_t n_pairs, const saloba_ksw_params* params, saloba_packing fmt, int32_t max_qlen,
+                      int32_t* out, void* workspace, size_t workspace_bytes, int64_t* status, void* stream);
 
 /* ---- end-to-end from host buffers ----------------------------------------------------------- */
 

@@ -16,6 +16,7 @@ import torch
 __all__ = [
     "LOCAL", "EXTEND", "PACK4", "PACK2", "Scoring", "Options", "BWA_MEM", "SalobaError", "lib", "lib_path",
     "packed_words", "pack", "workspace_bytes", "align_batch", "align", "align_banded", "start_workspace_bytes", "locate_start", "partition", "scatter_results",
+    "KswParams", "BWA_KSW", "ksw_extend", "ksw_align", "KSW_FIELDS",
     "align_host", "version", "EXPORTS",
 ]
 
@@ -27,6 +28,7 @@ OK, EINVAL, ECUDA, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4
 EXPORTS = ("saloba_packed_words", "saloba_pack", "saloba_workspace_bytes", "saloba_align_batch",
            "saloba_align_banded", "saloba_start_workspace_bytes", "saloba_locate_start",
            "saloba_partition_workspace_bytes", "saloba_partition", "saloba_scatter_results",
+           "saloba_ksw_workspace_bytes", "saloba_ksw_extend",
            "saloba_host_ctx_create", "saloba_host_ctx_destroy", "saloba_align_host_ctx", "saloba_align_host",
            "saloba_strerror", "saloba_version", "saloba_kernel_launches")
 
@@ -46,6 +48,10 @@ class SalobaError(RuntimeError):
 class _Scoring(ctypes.Structure):
     _fields_ = [("match", ctypes.c_int32), ("mismatch", ctypes.c_int32), ("gap_open", ctypes.c_int32),
                 ("gap_extend", ctypes.c_int32)]
+
+
+class _KswParams(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int32) for k in ("a", "b", "o_del", "e_del", "o_ins", "e_ins", "w", "end_bonus", "zdrop")]
 
 
 class _Options(ctypes.Structure):
@@ -70,6 +76,32 @@ class Scoring:
 
 #: BWA-MEM-style scoring of the BASELINE configs: match 1, mismatch -4, o=6 e=1 -> alpha 7, beta 1
 BWA_MEM = Scoring(1, -4, 7, 1)
+
+
+@dataclass(frozen=True)
+class KswParams:
+    """BWA-MEM extension parameters (saloba_ksw_params): b is the mismatch PENALTY (> 0); a gap of k
+    bases costs o + k*e; zdrop 0 disables the z-drop."""
+
+    a: int = 1
+    b: int = 4
+    o_del: int = 6
+    e_del: int = 1
+    o_ins: int = 6
+    e_ins: int = 1
+    w: int = 100
+    end_bonus: int = 5
+    zdrop: int = 100
+
+    def _c(self) -> _KswParams:
+        return _KswParams(self.a, self.b, self.o_del, self.e_del, self.o_ins, self.e_ins, self.w, self.end_bonus,
+                          self.zdrop)
+
+
+#: BWA-MEM's defaults (mem_opt_init)
+BWA_KSW = KswParams()
+#: rows of saloba_ksw_extend's output
+KSW_FIELDS = ("score", "qle", "tle", "gtle", "gscore", "max_off", "clip")
 
 
 @dataclass(frozen=True)
@@ -119,6 +151,11 @@ def lib() -> ctypes.CDLL:
         L.saloba_partition_workspace_bytes.restype = ctypes.c_size_t
         L.saloba_partition.argtypes = [vp, vp, i64, i32, vp, vp, ctypes.c_size_t, vp]
         L.saloba_partition.restype = ctypes.c_int
+        L.saloba_ksw_workspace_bytes.argtypes = [i64, i32, ctypes.c_int]
+        L.saloba_ksw_workspace_bytes.restype = ctypes.c_size_t
+        L.saloba_ksw_extend.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, ctypes.POINTER(_KswParams), ctypes.c_int, i32,
+                                        vp, vp, ctypes.c_size_t, vp, vp]
+        L.saloba_ksw_extend.restype = ctypes.c_int
         L.saloba_scatter_results.argtypes = [vp, vp, i64, i32, i64, vp, vp, vp, vp, vp]
         L.saloba_scatter_results.restype = ctypes.c_int
         L.saloba_start_workspace_bytes.argtypes = [i64, i64, i64, i32, ctypes.c_int]
@@ -297,6 +334,42 @@ def scatter_results(parts: torch.Tensor, index: torch.Tensor, n_total: int, out:
     _check(lib().saloba_scatter_results(_p(parts), _p(index), stride, world, n_total, _p(out[0]), _p(out[1]),
                                         _p(out[2]), _p(status), _stream(stream)), "saloba_scatter_results")
     return out, status
+
+
+def ksw_extend(q_words, q_word_off, q_len, t_words, t_word_off, t_len, h0, params: KswParams = BWA_KSW,
+               fmt: int = PACK4, max_qlen: int | None = None, out=None, workspace=None, stream=None):
+    """BWA-MEM-compatible extension of packed pairs (saloba_ksw_extend): returns (out int32[7, n]
+    with rows KSW_FIELDS, status)."""
+    n = q_len.numel()
+    dev = q_len.device
+    args = [_dev_tensor(a_, d_, nm) for a_, d_, nm in zip(
+        (q_words, q_word_off, q_len, t_words, t_word_off, t_len, h0),
+        (torch.int32, torch.int64, torch.int32, torch.int32, torch.int64, torch.int32, torch.int32),
+        ("q_words", "q_word_off", "q_len", "t_words", "t_word_off", "t_len", "h0"))]
+    if max_qlen is None:
+        max_qlen = int(args[2].max().item()) if n > 0 else 1
+    if out is None:
+        out = torch.empty((7, max(n, 1)), dtype=torch.int32, device=dev)
+    if workspace is None:
+        b = int(lib().saloba_ksw_workspace_bytes(n, max_qlen, dev.index))
+        if b == 0:
+            raise SalobaError(ECUDA, "saloba_ksw_workspace_bytes")
+        workspace = torch.empty(b, dtype=torch.uint8, device=dev)
+    status = torch.empty(1, dtype=torch.int64, device=dev)
+    pc = params._c()
+    rc = lib().saloba_ksw_extend(*[_p(a_) for a_ in args], n, ctypes.byref(pc), fmt, max_qlen, _p(out), _p(workspace),
+                                 workspace.numel(), _p(status), _stream(stream))
+    _check(rc, "saloba_ksw_extend")
+    return out[:, :n], status
+
+
+def ksw_align(q_ascii, q_off, t_ascii, t_off, h0, params: KswParams = BWA_KSW, fmt: int = PACK4,
+              max_qlen: int | None = None, stream=None):
+    """Device-resident ASCII pairs -> (out int32[7, n], status, q pack status, t pack status)."""
+    qw, qwo, ql, qst = pack(q_ascii, q_off, fmt, stream=stream)
+    tw, two, tl, tst = pack(t_ascii, t_off, fmt, stream=stream)
+    out, st = ksw_extend(qw, qwo[:-1], ql, tw, two[:-1], tl, h0, params, fmt, max_qlen=max_qlen, stream=stream)
+    return out, st, qst, tst
 
 
 def start_workspace_bytes(n_pairs: int, q_words_total: int, t_words_total: int, max_qlen: int,

@@ -26,6 +26,17 @@ void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cu
 const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt, int rows);
 const void* dp_i16_qn_kernel_ptr(int mode, int rows, int gidx);
 void launch_dp_i16_qn(int mode, int gidx, int grid, const AlignArgs& a, cudaStream_t s);
+const void* dp_g1_kernel_ptr(int mode, int fmt, bool qn);
+int g1_threads();
+int64_t g1_scratch_words(int64_t qcap);
+void launch_dp_g1(int mode, int grid, const AlignArgs& a, int bin, bool qn, cudaStream_t s);
+// the G = 1 int16x2 bins run the dedicated kernel of dp_g1.cu (16-row strips); 8-row strips
+// (Options.i16_rows = 8) and builds with SALOBA_G1_LEGACY keep the generic dp_i16 kernel
+#ifdef SALOBA_G1_LEGACY
+static bool use_g1(int) { return false; }
+#else
+static bool use_g1(int rows) { return rows != 8; }
+#endif
 void launch_reverse_prefix(int fmt, const uint32_t* words, const int64_t* word_off, const int32_t* end,
                            const int32_t* score, int64_t n, uint32_t* out, int32_t* out_len, int sms, cudaStream_t s);
 void launch_start_finalize(const int32_t* score, const int32_t* q_end, const int32_t* t_end, const int32_t* rscore,
@@ -42,6 +53,7 @@ struct DevInfo {
     int blocks_i32[2][NGROUPS] = {};
     int blocks_i16[2][2][NGROUPS] = {};  // [rows 8|16][mode][gidx]
     int blocks_i16qn[2][2][2] = {};      // QN variant: [rows 8|16][mode][G = 1|2]
+    int blocks_g1[2][2] = {};            // dp_g1 kernel: [mode][QN]
     int max_blocks_per_sm = 1;           // max resident blocks of any DP kernel (block-slot pool)
     cudaStream_t aux[4] = {};            // bins run as concurrent kernels on these
 };
@@ -83,6 +95,14 @@ static const DevInfo* dev_info(int device) {
                 }
             }
         for (int mode = 0; mode < 2; ++mode)
+            for (int qn = 0; qn < 2; ++qn) {
+                int nb = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_g1_kernel_ptr(mode, SALOBA_PACK4, qn != 0),
+                                                              g1_threads(), 0);
+                d.blocks_g1[mode][qn] = std::max(1, nb);
+                d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_g1[mode][qn]);
+            }
+        for (int mode = 0; mode < 2; ++mode)
             for (int g = 0; g < NGROUPS; ++g) {
                 d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_i32[mode][g]);
                 for (int ri = 0; ri < 2; ++ri) {
@@ -113,6 +133,7 @@ struct Layout {
 };
 
 static int grid_for(const DevInfo* d, int mode, int path, int g, int rows = 16) {
+    if (path == PATH_I16 && g == 0 && use_g1(rows)) return d->sms * d->blocks_g1[mode][0];
     return d->sms * (path == PATH_I16 ? d->blocks_i16[rows == 8 ? 0 : 1][mode][g] : d->blocks_i32[mode][g]);
 }
 static int threads_for(int path) { return path == PATH_I16 ? I16_THREADS : BLOCK_THREADS; }
@@ -123,7 +144,9 @@ static int rows_for(int path) { return path == PATH_I16 ? 8 : 4; }
 static int64_t block_need_words(int path, int g, int64_t Qmax) {
     const int64_t G = int64_t(1) << g;
     const int64_t q = std::min<int64_t>(qmax_for_gidx(g), Qmax);
-    return int64_t(threads_for(path)) / G * rows_for(path) * (8 * q + 8);
+    const int64_t generic = int64_t(threads_for(path)) / G * rows_for(path) * (8 * q + 8);
+    // G = 1 int16x2 bins: the dp_g1 kernel's selector + spill scratch (dp_g1.cu), or the generic one
+    return path == PATH_I16 && g == 0 ? std::max(generic, g1_scratch_words(q)) : generic;
 }
 static int64_t block_slot_words(int64_t Qmax) {
     int64_t w = 0;
@@ -303,6 +326,10 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
                     AlignArgs a16 = a;
                     a16.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(g - 1), Qsup) + 8;
                     launch_dp_i16(int(mode), g - 1, grid_for(d, int(mode), path, g - 1, i16_rows), a16, LONG_BIN, as);
+                } else if (path == PATH_I16 && g == 0 && use_g1(i16_rows)) {
+                    AlignArgs a1 = a;
+                    a1.spill_stride = std::min<int64_t>(qmax_for_gidx(0), Qsup);  // dp_g1: query-block capacity
+                    launch_dp_g1(int(mode), grid_for(d, int(mode), path, g, i16_rows), a1, path * 8 + g, false, as);
                 } else if (path == PATH_I16)
                     launch_dp_i16(int(mode), g, grid_for(d, int(mode), path, g, i16_rows), a, path * 8 + g, as);
                 else
@@ -315,6 +342,12 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
         }
         if (fmt == SALOBA_PACK4) {  // QN bins: int16x2 G=1 / G=2 pairs whose query contains N
             for (int g = 0; g <= 1; ++g) {
+                if (g == 0 && use_g1(i16_rows)) {
+                    AlignArgs a1 = a;
+                    a1.spill_stride = std::min<int64_t>(qmax_for_gidx(0), Qsup);
+                    launch_dp_g1(int(mode), d->sms * d->blocks_g1[int(mode)][1], a1, QN_BIN, true, aux[(j + g) % NAUX]);
+                    continue;
+                }
                 a.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(g), Qsup) + 8;
                 launch_dp_i16_qn(int(mode), g, d->sms * d->blocks_i16qn[i16_rows == 8 ? 0 : 1][int(mode)][g], a,
                                  aux[(j + g) % NAUX]);

@@ -1,0 +1,517 @@
+// dp_g1.cu — A3 for short reads: the int16x2 pair-SIMD DP kernel at subwarp size G = 1.
+//
+// The scheduler sends every int16x2 pair whose cost model prefers one lane per pair here (config 2:
+// all 1M pairs; most of configs 3 and 5).  Same method as dp_i16.cu (§IV-A, P:579-642;
+// Eqs. 1-3; two exact passes), specialised for G = 1, where every 16-row
+// strip of the target is a chunk of its own and the only inter-strip boundary is the thread's OWN
+// spilled bottom row:
+//
+//   * no shuffles and no Q+G-1 ramp: a chunk is Q steps of one 8-column block each;
+//   * PRMT selectors are built once per pair-duo (during chunk 0, from the packed query words) and
+//     stored to the thread's scratch; later chunks and pass 2 fetch 8 ready selector words per step
+//     (saves ~30 ALU instructions per step = ~5% of the step's ALU work);
+//   * every global stream is laid out [.. block w ..][quad][thread] so that one warp-wide 16-byte
+//     access covers 512 contiguous bytes (coalesced spill stores, cp.async stage loads);
+//   * the shared-memory stage is [slot][quad][thread]: conflict-free LDS.128;
+//   * top-row values are read from the stage per column and bottom-row values stored per column
+//     pair, so neither row is held in registers across a step (<= 128 registers: 4 blocks / SM);
+//   * pass 2 tests a candidate column's 16 rows in registers (no local-memory parking).
+//
+// Cell update per 32-bit register (2 cells, one per pair of the duo): see dp_i16.cu.
+// Exactness of the 16-bit lanes is guaranteed by routing (schedule.cu): scores fit int8 and all
+// H, E, F stay inside int16 (SURVEY §8(c) reading 8).
+#include "dp_i16_common.cuh"
+
+namespace saloba {
+
+constexpr int G1_T = 128;    // threads per block
+constexpr int G1_R = 16;     // target rows per strip (two packed target words per half)
+constexpr int G1_DEPTH = 3;  // stage slots in pass 1 (inputs requested two steps ahead)
+constexpr int G1_NBUF = 4;   // spill buffers per thread: read, write, two checkpoints
+// Resident blocks per SM.  Not register-bound: the spill rows of all resident threads must stay
+// L2-resident between a chunk writing them and the next chunk reading them (reuse distance =
+// resident threads x Q x 64 B, + the selector stream); measured on B200 (config 2): 4 blocks/SM
+// pushed that past the 126 MB L2 (L2 hit rate 63% -> 21%, DRAM reads 6x) and ran 35% slower.
+#ifndef G1_MINB
+#define G1_MINB 3
+#endif
+// G1_PIPE: read a step's first shared-memory inputs at the end of the previous step (1) or at its
+// head (0).  G1_BOTREG: keep the chunk-bottom row in registers and store it after the step (1) or
+// store each column pair as it is produced (0).
+#ifndef G1_PIPE
+#define G1_PIPE 0
+#endif
+#ifndef G1_BOTREG
+#define G1_BOTREG 0
+#endif
+
+// Scratch words per thread per query block: 8 selector words (4 compact ones when the query has
+// no N) + G1_NBUF spill rows of 16 words.
+__host__ __device__ constexpr int g1_words_per_block() { return 8 + G1_NBUF * 16; }
+
+struct G1Stage {
+    uint4 sel[G1_DEPTH][2][G1_T];   // chunks >= 1 and pass 2: the step's selectors (QN: 8 words
+                                    // with N flags; otherwise [0] holds 8 compact 16-bit selectors)
+    uint32_t q[G1_DEPTH][2][G1_T];  // chunk 0: the step's packed query words (halves A, B)
+    uint4 top[4][4][G1_T];          // top-row quads (H[2q], F[2q], H[2q+1], F[2q+1]);
+                                    // pass 1: slots 0..2; pass 2: A slots 0..1, B slots 2..3
+};
+
+// Scratch of one thread slot inside the block's pool slot:
+//   sel  [Qcap][2][G1_T] uint4          PRMT selectors per query block: 8 x 16 bits in [w][0]
+//                                       (QN: 8 words with N flags in bytes 2-3, [w][0..1]); all
+//                                       lanes use the same w at once: a warp's load is 512
+//                                       contiguous bytes
+//   row  [G1_T][G1_NBUF][Qcap][4] uint4 spilled chunk-bottom rows (H, F of 8 columns), contiguous
+//                                       per thread.  The buffer rotation differs from lane to lane
+//                                       (it follows each lane's checkpoints), so a [buf][w][q][thread]
+//                                       interleave (G1_ROWS_INTERLEAVED) shares every 128-byte line
+//                                       between lanes on different buffers: measured on B200 it
+//                                       partially wrote lines of dead rows and cut the L2 hit rate
+//                                       from 63% to 18% (DRAM reads 5x).
+#ifndef G1_ROWS_INTERLEAVED
+#define G1_ROWS_INTERLEAVED 0
+#endif
+struct G1Scratch {
+    uint4* sel;
+    uint4* row;
+    int qcap;
+    __device__ __forceinline__ uint4* sel_at(int w, int h) const { return sel + (size_t(w) * 2 + h) * G1_T + threadIdx.x; }
+    __device__ __forceinline__ uint4* row_at(int buf, int w, int q) const {
+#if G1_ROWS_INTERLEAVED
+        return row + ((size_t(buf) * qcap + w) * 4 + q) * G1_T + threadIdx.x;
+#else
+        return row + ((size_t(threadIdx.x) * G1_NBUF + buf) * qcap + w) * 4 + q;
+#endif
+    }
+};
+
+// L2 residency of the spill rows (G1_HINT): 0 = default policy; 1 = top-row reads marked
+// evict-first (a row is dead once the next chunk has read it); 2 = also bottom-row writes marked
+// evict-last (keep them until that read)
+#ifndef G1_HINT
+#define G1_HINT 0
+#endif
+__device__ __forceinline__ uint64_t l2_policy(bool last) {
+    uint64_t p;
+    if (last) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_pred16(uint4* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, bool on) {
+#if G1_HINT >= 2
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+                 "setp.ne.b32 p, %5, 0;\n\t@p st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, pol;\n\t}"
+                 ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d), "r"(int(on)));
+#else
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t@p st.global.v4.u32 [%0], {%1, %2, %3, %4};\n\t}"
+                 ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d), "r"(int(on)));
+#endif
+}
+
+// the 4 raw packed target words of a strip starting at rows rA / rB (2 per half)
+template <int FMT>
+__device__ __forceinline__ void g1_target_raw(const HalfInfo& A, const HalfInfo& B, const uint32_t* twA,
+                                              const uint32_t* twB, int rA, int rB, uint32_t (&raw)[4]) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int ba = (rA >> 3) + i, bb = (rB >> 3) + i;
+        raw[i] = (8 * ba < A.m) ? __ldg(twA + (FMT == SALOBA_PACK2 ? (ba >> 1) : ba)) : 0u;
+        raw[2 + i] = (8 * bb < B.m) ? __ldg(twB + (FMT == SALOBA_PACK2 ? (bb >> 1) : bb)) : 0u;
+    }
+}
+
+// One 16-row strip of both halves.
+//   PASS2 = false: returns the lane's maximum of the diagonal candidates D over the strip (max H =
+//     max(0, max D): a positive H reached through a gap is strictly below an earlier cell).
+//   PASS2 = true: records the first cell (row-major) equal to `target` per half into hit[].
+//   selgen: build the selectors from the query words and store them (chunk 0 of pass 1).
+//   topA / topB: spill buffer of the top row per half (-1: the table boundary); bot: buffer that
+//     receives the bottom row (-1: none).
+template <int MODE, int FMT, bool PASS2, bool QN>
+__device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, const HalfInfo& A, const HalfInfo& B,
+                                             const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
+                                             const int rA, const int rB, const int topA, const int topB,
+                                             const int bot, const bool selgen, const uint32_t target,
+                                             int (&hit)[4], G1Stage& st, const G1Scratch& sc,
+                                             const uint32_t (&twraw)[4]) {
+    const int tid = threadIdx.x;
+    const int al = a.alpha, be = a.beta;
+    const uint32_t nbeta = pack2(-be, -be), nalpha = pack2(-al, -al), noGap = pack2(-al - be, -al - be);
+    const uint32_t mmw = pack2(a.mismatch, a.mismatch);  // QN: substitution of an N column
+    uint32_t lam = 2;
+    while (int(lam) < a.match + 1) lam <<= 1;
+    uint32_t tabA[G1_R], tabB[G1_R];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const uint32_t ta = staged_codes<FMT>(twraw[i], (rA >> 3) + i, A.m);
+        const uint32_t tb = staged_codes<FMT>(twraw[2 + i], (rB >> 3) + i, B.m);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            tabA[8 * i + r] = row_table((ta >> (4 * r)) & 15u, a.match, a.mismatch);
+            tabB[8 * i + r] = row_table((tb >> (4 * r)) & 15u, a.match, a.mismatch);
+        }
+    }
+    // Left boundary H(i,-1) and E one column ahead (E(i,-1) as "no gap": only non-positive E values
+    // change, which never reach H = max(0, ...)); corner H(r0-1, -1).
+    uint32_t Hl[G1_R], En[G1_R];
+#pragma unroll
+    for (int r = 0; r < G1_R; ++r) {
+        const int ha = MODE ? max(0, A.h0 - al - be * (rA + r)) : 0;
+        const int hb = MODE ? max(0, B.h0 - al - be * (rB + r)) : 0;
+        Hl[r] = pack2(ha, hb);
+        En[r] = vadd(Hl[r], nalpha);
+    }
+    uint32_t corner;
+    {
+        const int ca = MODE ? (rA == 0 ? A.h0 : max(0, A.h0 - al - be * (rA - 1))) : 0;
+        const int cb = MODE ? (rB == 0 ? B.h0 : max(0, B.h0 - al - be * (rB - 1))) : 0;
+        corner = pack2(ca, cb);
+    }
+    uint32_t M0 = 0, M1 = 0, M2 = 0, M3 = 0;
+    constexpr int DEPTH = PASS2 ? 2 : G1_DEPTH;
+    const bool topA_mem = topA >= 0;
+    const bool topB_mem = PASS2 && topB >= 0 && topB != topA;
+    const bool split = PASS2 && (topB != topA || rB != rA);  // pass 2 halves at different chunks
+#if G1_HINT >= 1
+    const uint64_t evict_first = l2_policy(false);
+#endif
+    auto prefetch = [&](int s2, int slot) {
+        if (s2 < Q) {
+            if (selgen) {
+                const int wi = FMT == SALOBA_PACK2 ? (s2 >> 1) : s2;
+                if (8 * s2 < A.n) cp_async4(&st.q[slot][0][tid], qwA + wi);
+                if (8 * s2 < B.n) cp_async4(&st.q[slot][1][tid], qwB + wi);
+            } else {
+                cp_async16(&st.sel[slot][0][tid], sc.sel_at(s2, 0));
+                if (QN) cp_async16(&st.sel[slot][1][tid], sc.sel_at(s2, 1));
+            }
+            if (topA_mem) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+#if G1_HINT >= 1
+                    if (!PASS2) cp_async16_hint(&st.top[slot][q][tid], sc.row_at(topA, s2, q), evict_first);
+                    else
+#endif
+                    cp_async16(&st.top[slot][q][tid], sc.row_at(topA, s2, q));
+                }
+            }
+            if (topB_mem) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) cp_async16(&st.top[2 + slot][q][tid], sc.row_at(topB, s2, q));
+            }
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int p = 0; p < DEPTH - 1; ++p) prefetch(p, p);
+    // Stage-in of step s2's inputs (slot `slot`): wait for its cp.async group, write table-boundary
+    // top rows into the slot, and read the step's first shared-memory values into registers.  It
+    // runs at the END of the previous step, so a step starts with its selectors and first top-row
+    // quad already in registers (no LDS latency at the head of the step).
+    uint32_t nq0 = 0, nq1 = 0;
+    uint4 nsel0 = make_uint4(0, 0, 0, 0), nsel1 = nsel0, ntq = nsel0, ntb = nsel0;
+    auto stage_in = [&](int s2, int slot) {
+        cp_async_wait<DEPTH - 2>();
+        if (!topA_mem) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = 8 * s2 + 2 * q;
+                const uint32_t h0v = pack2(MODE ? max(0, A.h0 - al - be * j) : 0, MODE ? max(0, B.h0 - al - be * j) : 0);
+                const uint32_t h1v = pack2(MODE ? max(0, A.h0 - al - be * (j + 1)) : 0,
+                                           MODE ? max(0, B.h0 - al - be * (j + 1)) : 0);
+                st.top[slot][q][tid] = make_uint4(h0v, noGap, h1v, noGap);
+            }
+        }
+        if (PASS2 && split && !topB_mem) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = 8 * s2 + 2 * q;
+                st.top[2 + slot][q][tid] = make_uint4(pack2(0, MODE ? max(0, B.h0 - al - be * j) : 0), noGap,
+                                                      pack2(0, MODE ? max(0, B.h0 - al - be * (j + 1)) : 0), noGap);
+            }
+        }
+        if (selgen) {
+            nq0 = st.q[slot][0][tid];
+            nq1 = st.q[slot][1][tid];
+        } else {
+            nsel0 = st.sel[slot][0][tid];
+            if (QN) nsel1 = st.sel[slot][1][tid];
+        }
+        ntq = st.top[slot][0][tid];
+        if (PASS2 && split) ntb = st.top[2 + slot][0][tid];
+    };
+    if (G1_PIPE) stage_in(0, 0);
+    int cur = 0;
+    for (int s = 0; s < Q; ++s) {
+        if (!G1_PIPE) stage_in(s, cur);
+        prefetch(s + DEPTH - 1, cur == 0 ? DEPTH - 1 : cur - 1);
+        uint32_t sel[8];
+        if (selgen) {
+            const uint32_t qcA = staged_codes<FMT>(nq0, s, A.n);
+            const uint32_t qcB = staged_codes<FMT>(nq1, s, B.n);
+            make_selectors(qcA, qcB, sel);
+            if constexpr (QN) {
+                // N columns (nibble 4): bytes 2 / 3 of the selector word set to 0xFF for half A / B;
+                // PRMT reads only the low 16 bits, the compute loop expands the flags to masks
+                const uint32_t vA = qcA ^ 0x44444444u, vB = qcB ^ 0x44444444u;
+                const uint32_t zA = ~(((vA & 0x77777777u) + 0x77777777u) | vA) & 0x88888888u;
+                const uint32_t zB = ~(((vB & 0x77777777u) + 0x77777777u) | vB) & 0x88888888u;
+#pragma unroll
+                for (int x = 0; x < 8; ++x)
+                    sel[x] = (sel[x] & 0xFFFFu) | (((zA >> (4 * x + 3)) & 1u) * 0x00FF0000u) |
+                             (((zB >> (4 * x + 3)) & 1u) * 0xFF000000u);
+            }
+            if (QN) {
+                *sc.sel_at(s, 0) = make_uint4(sel[0], sel[1], sel[2], sel[3]);
+                *sc.sel_at(s, 1) = make_uint4(sel[4], sel[5], sel[6], sel[7]);
+            } else {  // compact: two 16-bit selectors per word (PRMT reads only the low 16 bits)
+                *sc.sel_at(s, 0) = make_uint4(prmt(sel[0], sel[1], 0x5410), prmt(sel[2], sel[3], 0x5410),
+                                              prmt(sel[4], sel[5], 0x5410), prmt(sel[6], sel[7], 0x5410));
+            }
+        } else if (QN) {
+            sel[0] = nsel0.x; sel[1] = nsel0.y; sel[2] = nsel0.z; sel[3] = nsel0.w;
+            sel[4] = nsel1.x; sel[5] = nsel1.y; sel[6] = nsel1.z; sel[7] = nsel1.w;
+        } else {
+            // odd columns: the high 16 bits, moved down by IMAD.HI (FMA pipe) to spare the ALU pipe
+            sel[0] = nsel0.x; sel[1] = __umulhi(nsel0.x, 0x10000u);
+            sel[2] = nsel0.y; sel[3] = __umulhi(nsel0.y, 0x10000u);
+            sel[4] = nsel0.z; sel[5] = __umulhi(nsel0.z, 0x10000u);
+            sel[6] = nsel0.w; sel[7] = __umulhi(nsel0.w, 0x10000u);
+        }
+        const int slot = cur;
+        cur = (cur == DEPTH - 1) ? 0 : cur + 1;
+        uint32_t hdiag_top = corner, prevH = 0, prevF = 0;
+#if G1_BOTREG
+        uint32_t botH[8], botF[8];
+#endif
+        // top-row quads: one conflict-free LDS.128 per column pair, issued a pair ahead
+        uint4 tq = ntq, tqn = ntq, tb = ntb, tbn = ntb;
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+            uint32_t hup, fup;
+            {
+                if (!(x & 1)) {
+                    tq = tqn;
+                    if (PASS2 && split) tb = tbn;
+                    if (x + 2 < 8) {
+                        tqn = st.top[slot][(x >> 1) + 1][tid];
+                        if (PASS2 && split) tbn = st.top[2 + slot][(x >> 1) + 1][tid];
+                    }
+                }
+                hup = (x & 1) ? tq.z : tq.x;
+                fup = (x & 1) ? tq.w : tq.y;
+                if (PASS2 && split) {  // high halves from half B's own checkpoint row
+                    hup = prmt(hup, (x & 1) ? tb.z : tb.x, 0x7610);
+                    fup = prmt(fup, (x & 1) ? tb.w : tb.y, 0x7610);
+                }
+            }
+            uint32_t haup = vadd(hup, nalpha);
+            uint32_t hdiag = hdiag_top;
+            hdiag_top = hup;
+            uint32_t nm = 0;
+            if constexpr (QN) nm = prmt(sel[x], 0u, 0x3322);  // 0xFFFF per half whose column is N
+            uint32_t dprev = 0;
+#pragma unroll
+            for (int r = 0; r < G1_R; ++r) {
+                const uint32_t f = vaddmax(fup, nbeta, haup);
+                const uint32_t e = En[r];
+                uint32_t scv = prmt(tabA[r], tabB[r], sel[x]);
+                if constexpr (QN) scv = (scv & ~nm) | (mmw & nm);
+                uint32_t d;
+                if (MODE) {
+                    // dead-zero (EXTEND): D = hdiag + s if hdiag > 0, else <= 0, as
+                    // min(hdiag + s, lambda * hdiag) with lambda = 2^k >= match + 1 (one IMAD
+                    // scales both halves: hdiag >= 0 and lambda * hdiag <= 32767 by routing)
+                    d = vaddmin(hdiag, scv, hdiag * lam);
+                } else {
+                    d = vadd(hdiag, scv);
+                }
+                const uint32_t h = vmax3relu(d, e, f);
+                const uint32_t ha = vadd(h, nalpha);
+                hdiag = Hl[r];
+                Hl[r] = h;
+                En[r] = vaddmax(e, nbeta, ha);
+                hup = h;
+                haup = ha;
+                fup = f;
+                if (!PASS2) {
+                    if (r & 1) {
+                        if ((r & 7) == 1) M0 = vmax3(M0, dprev, d);
+                        if ((r & 7) == 3) M1 = vmax3(M1, dprev, d);
+                        if ((r & 7) == 5) M2 = vmax3(M2, dprev, d);
+                        if ((r & 7) == 7) M3 = vmax3(M3, dprev, d);
+                    }
+                    dprev = d;
+                }
+            }
+            // chunk-bottom row -> spill, one 16-byte store per column pair (predicated, not branched,
+            // so the step stays one basic block)
+#if G1_BOTREG
+            botH[x] = hup;
+            botF[x] = fup;
+#else
+            if (x & 1) st_pred16(sc.row_at(bot < 0 ? 0 : bot, s, x >> 1), prevH, prevF, hup, fup, bot >= 0);
+            prevH = hup;
+            prevF = fup;
+#endif
+            if (PASS2) {
+                // a cell can only equal `target` (the pair maximum) where the column maximum reaches it;
+                // such columns are rare (about one per pair): test their rows in registers
+                uint32_t cm = vmax3(vmax3(Hl[0], Hl[1], Hl[2]), vmax3(Hl[3], Hl[4], Hl[5]), vmax3(Hl[6], Hl[7], Hl[8]));
+                cm = vmax3(cm, vmax3(Hl[9], Hl[10], Hl[11]), vmax3(Hl[12], Hl[13], Hl[14]));
+                cm = vmax(cm, Hl[15]);
+                if (lo16(cm) >= lo16(target) || hi16(cm) >= hi16(target)) {
+                    uint32_t bits = 0;
+#pragma unroll
+                    for (int r = 0; r < G1_R; ++r) bits |= eq_bits(Hl[r], target, r);
+                    take_hit(bits, 8 * s + x, rA, rB, hit);
+                }
+            }
+        }
+        corner = hdiag_top;
+        if (G1_PIPE && s + 1 < Q) stage_in(s + 1, cur);
+#if G1_BOTREG
+        if (bot >= 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                *sc.row_at(bot, s, q) = make_uint4(botH[2 * q], botF[2 * q], botH[2 * q + 1], botF[2 * q + 1]);
+        }
+#endif
+    }
+    return vmax(vmax(M0, M1), vmax(M2, M3));
+}
+
+template <int MODE, int FMT, bool QN>
+__global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int bin) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int start = a.bin_start[bin];
+    const int cnt = a.bin_start[bin + 1] - start;
+    const int items = (cnt + 1) >> 1;  // pair-duos
+    // blocks the bin cannot use exit before claiming a scratch slot (empty bins: every block)
+    if (int64_t(blockIdx.x) * G1_T >= int64_t(items)) return;
+    const int bslot = acquire_block_slot(a.slot_bitmap, a.slot_words);
+    G1Scratch sc;
+    sc.qcap = int(a.spill_stride);
+    {
+        uint4* pool = reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(a.spill) + bslot * a.block_slot_words);
+        sc.sel = pool;
+        sc.row = pool + size_t(sc.qcap) * 2 * G1_T;
+    }
+    __shared__ G1Stage st;
+
+    for (;;) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(a.bin_counter + bin, 32);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= items) break;
+        const int item = base + lane;
+        const bool has = item < items;
+        HalfInfo A, B;
+        A.p = has ? int(a.perm[start + 2 * item]) : -1;
+        B.p = (has && 2 * item + 1 < cnt) ? int(a.perm[start + 2 * item + 1]) : -1;
+        A.n = A.p >= 0 ? a.q_len[A.p] : 0;
+        A.m = A.p >= 0 ? a.t_len[A.p] : 0;
+        A.h0 = (MODE && A.p >= 0) ? a.h0[A.p] : 0;
+        B.n = B.p >= 0 ? a.q_len[B.p] : 0;
+        B.m = B.p >= 0 ? a.t_len[B.p] : 0;
+        B.h0 = (MODE && B.p >= 0) ? a.h0[B.p] : 0;
+        const uint32_t* qwA = A.p >= 0 ? a.q_words + a.q_word_off[A.p] : a.q_words;
+        const uint32_t* twA = A.p >= 0 ? a.t_words + a.t_word_off[A.p] : a.t_words;
+        const uint32_t* qwB = B.p >= 0 ? a.q_words + a.q_word_off[B.p] : qwA;
+        const uint32_t* twB = B.p >= 0 ? a.t_words + a.t_word_off[B.p] : twA;
+        const int Qi = (max(A.n, B.n) + 7) >> 3;
+        const int chunks = max((A.m + G1_R - 1) / G1_R, (B.m + G1_R - 1) / G1_R);
+        const int Q = int(__reduce_max_sync(FULL, unsigned(Qi)));  // warp-uniform loop bounds
+        const int chunks_w = int(__reduce_max_sync(FULL, unsigned(chunks)));
+
+        // pass 1 -------------------------------------------------------------------------------
+        const int floorA = MODE ? A.h0 : 0, floorB = MODE ? B.h0 : 0;
+        int bestA = floorA, bestB = floorB;  // running maxima (strict improvement records the chunk)
+        int ckA = -1, ckB = -1;              // chunk holding the first maximum (-1: none above floor)
+        int bufA = -1, bufB = -1;            // buffer holding that chunk's top row (-1: boundary)
+        int rd = -1, wr = 0;
+        uint32_t twn[4];
+        g1_target_raw<FMT>(A, B, twA, twB, 0, 0, twn);
+        for (int c = 0; c < chunks_w; ++c) {
+            uint32_t twc[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) twc[i] = twn[i];
+            if (c + 1 < chunks_w) g1_target_raw<FMT>(A, B, twA, twB, (c + 1) * G1_R, (c + 1) * G1_R, twn);
+            const bool last = (c + 1 >= chunks);
+            int dummy[4];
+            const uint32_t m = g1_strip<MODE, FMT, false, QN>(a, Q, A, B, qwA, qwB, c * G1_R, c * G1_R, rd, rd,
+                                                              last ? -1 : wr, c == 0, 0u, dummy, st, sc, twc);
+            if (c < chunks) {
+                if (lo16(m) > bestA) {
+                    bestA = lo16(m);
+                    ckA = c;
+                    bufA = rd;
+                }
+                if (hi16(m) > bestB) {
+                    bestB = hi16(m);
+                    ckB = c;
+                    bufB = rd;
+                }
+            }
+            if (!last) {
+                rd = wr;
+                int nw = 0;  // next write buffer: not the new read buffer nor a live checkpoint
+                while (nw == rd || nw == bufA || nw == bufB) ++nw;
+                wr = nw;
+            }
+        }
+        // pass 2 -------------------------------------------------------------------------------
+        int hit[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
+        const bool need2 = ckA >= 0 || ckB >= 0;
+        if (__any_sync(FULL, need2)) {
+            const int cA = ckA >= 0 ? ckA : (ckB >= 0 ? ckB : 0), cB = ckB >= 0 ? ckB : cA;
+            const int bA = ckA >= 0 ? bufA : (ckB >= 0 ? bufB : -1), bB = ckB >= 0 ? bufB : bA;
+            const uint32_t target = pack2(ckA >= 0 ? bestA : 0x7FFF, ckB >= 0 ? bestB : 0x7FFF);
+            uint32_t tw2[4];
+            g1_target_raw<FMT>(A, B, twA, twB, cA * G1_R, cB * G1_R, tw2);
+            g1_strip<MODE, FMT, true, QN>(a, Q, A, B, qwA, qwB, cA * G1_R, cB * G1_R, bA, bB, -1, false, target, hit,
+                                         st, sc, tw2);
+        }
+        __syncwarp(FULL);
+        if (A.p >= 0) {
+            const int z = MODE ? -1 : 0;
+            a.score[A.p] = bestA;
+            a.t_end[A.p] = ckA >= 0 ? (hit[0] == INT_MAX ? -3 : hit[0]) : z;
+            a.q_end[A.p] = ckA >= 0 ? (hit[1] == INT_MAX ? -3 : hit[1]) : z;
+            if (B.p >= 0) {
+                a.score[B.p] = bestB;
+                a.t_end[B.p] = ckB >= 0 ? (hit[2] == INT_MAX ? -3 : hit[2]) : z;
+                a.q_end[B.p] = ckB >= 0 ? (hit[3] == INT_MAX ? -3 : hit[3]) : z;
+            }
+        }
+    }
+    release_block_slot(a.slot_bitmap, bslot);
+}
+
+template <int MODE>
+static const void* g1_ptr(int fmt, bool qn) {
+    if (qn) return (const void*)dp_g1_kernel<MODE, SALOBA_PACK4, true>;
+    return fmt == SALOBA_PACK2 ? (const void*)dp_g1_kernel<MODE, SALOBA_PACK2, false>
+                               : (const void*)dp_g1_kernel<MODE, SALOBA_PACK4, false>;
+}
+const void* dp_g1_kernel_ptr(int mode, int fmt, bool qn) {
+    return mode == SALOBA_EXTEND ? g1_ptr<1>(fmt, qn) : g1_ptr<0>(fmt, qn);
+}
+int g1_threads() { return G1_T; }
+int64_t g1_scratch_words(int64_t qcap) { return int64_t(G1_T) * g1_words_per_block() * qcap; }
+
+void launch_dp_g1(int mode, int grid, const AlignArgs& a, int bin, bool qn, cudaStream_t s) {
+    const void* fn = dp_g1_kernel_ptr(mode, a.fmt, qn);
+    AlignArgs args = a;
+    void* params[] = {&args, &bin};
+    cudaLaunchKernel(fn, dim3(grid), dim3(G1_T), params, 0, s);
+    count_launches(1);
+}
+
+}  // namespace saloba

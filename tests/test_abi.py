@@ -151,3 +151,27 @@ def test_host_checked_errors_scatter_results(L):
     assert L.saloba_scatter_results(dummy, dummy, -1, 2, 20, dummy, dummy, dummy, dummy, nul) == sb.EINVAL
     assert L.saloba_scatter_results(dummy, dummy, 10, 2, 20, nul, dummy, dummy, dummy, nul) == sb.EINVAL  # no output
     assert L.saloba_scatter_results(dummy, dummy, 10, 2, 1 << 31, dummy, dummy, dummy, dummy, nul) == sb.EINVAL
+
+
+def test_host_checked_errors_ksw(L):
+    """saloba_ksw_extend (NEXT-1): argument errors are returned before any CUDA call."""
+    import paper_2301_09310_b200 as sb
+
+    nul = ctypes.c_void_p(0)
+    dummy = ctypes.c_void_p(256)
+    good = sb.BWA_KSW._c()
+    args = [dummy] * 7 + [10, ctypes.byref(good), 4, 150, dummy, dummy, 1 << 20, dummy, nul]
+    a = list(args); a[14] = nul  # status
+    assert L.saloba_ksw_extend(*a) == sb.EINVAL
+    a = list(args); a[6] = nul  # h0
+    assert L.saloba_ksw_extend(*a) == sb.EINVAL
+    a = list(args); a[9] = 3  # fmt
+    assert L.saloba_ksw_extend(*a) == sb.EINVAL
+    a = list(args); a[12] = ctypes.c_void_p(300)  # unaligned workspace
+    assert L.saloba_ksw_extend(*a) == sb.EINVAL
+    for bad in (sb.KswParams(a=0), sb.KswParams(b=0), sb.KswParams(e_ins=0), sb.KswParams(w=-1),
+                sb.KswParams(zdrop=-1), sb.KswParams(o_del=2000)):
+        a = list(args); a[8] = ctypes.byref(bad._c())
+        assert L.saloba_ksw_extend(*a) == sb.EINVAL, bad
+    a = list(args); a[8] = None
+    assert L.saloba_ksw_extend(*a) == sb.EINVAL
