@@ -62,6 +62,8 @@ def parse():
                     help="skip timing the step replayed from a CUDA graph (N=1 extra key cuda_graph)")
     ap.add_argument("--band", type=int, default=-1, help="NEXT-2: also time saloba_align_banded with this w")
     ap.add_argument("--band-steps", type=int, default=3)
+    ap.add_argument("--ksw-steps", type=int, default=3,
+                    help="NEXT-1: time saloba_ksw_extend (BWA-MEM defaults) on the same packed batch (0: skip)")
     ap.add_argument("--partition", default="balanced", choices=["balanced", "equal"],
                     help="N>1: length-balanced (saloba_partition) or the paper's equal contiguous split")
     ap.add_argument("--force-group", type=int, default=0)
@@ -502,6 +504,31 @@ def main():
                   "launches_per_call": (sb.kernel_launches() - l0) // args.band_steps,
                   "api": "saloba_align_banded (exact int32 kernel, band-limited step ranges)"}
 
+    # ---- NEXT-1: BWA-MEM-compatible extension over the same packed batch (saloba_ksw_extend) ----
+    ksw = None
+    if args.ksw_steps > 0:
+        n_ = al.n
+        kout = torch.empty((7, n_), dtype=torch.int32, device=dev)
+        kws = torch.empty(int(sb.lib().saloba_ksw_workspace_bytes(n_, max_q, dev.index)), dtype=torch.uint8,
+                          device=dev)
+        kargs = (al.q_words, al.q_word_off[:-1], al.q_len[:n_], al.t_words, al.t_word_off[:-1], al.t_len[:n_], h0,
+                 sb.BWA_KSW, sb.PACK4)
+        _, kst = sb.ksw_extend(*kargs, max_qlen=max_q, out=kout, workspace=kws)  # warm
+        torch.cuda.synchronize()
+        assert int(kst.item()) == -1
+        l0 = sb.kernel_launches()
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
+        for _ in range(args.ksw_steps):
+            sb.ksw_extend(*kargs, max_qlen=max_q, out=kout, workspace=kws)
+        k1.record(stream)
+        torch.cuda.synchronize()
+        kms = k0.elapsed_time(k1) / args.ksw_steps
+        ksw = {"ms_per_call": round(kms, 3), "gcups_full_table": round(cells_rank / (kms * 1e-3) / 1e9, 2),
+               "launches_per_call": (sb.kernel_launches() - l0) // args.ksw_steps,
+               "params": "BWA-MEM defaults a1 b4 o6 e1 w100 end_bonus5 zdrop100, h0 = the batch's seed scores",
+               "api": "saloba_ksw_extend (ksw_extend2 semantics: band, row trimming, z-drop, gscore; warp-per-pair row sweep)"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -556,7 +583,7 @@ def main():
                    "partition": partition_desc, "measured_rank_balance_max_over_mean": balance,
                    "gen_seconds": round(gen_s, 1)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-        "start_pass": start_pass, "banded": banded, "cuda_graph": graph,
+        "start_pass": start_pass, "banded": banded, "ksw_extend": ksw, "cuda_graph": graph,
         "clocks": {"sm_mhz": csum["sm_mhz"], "sm_max_mhz": csum["sm_max_mhz"], "reasons": csum["reasons"]},
     }
     print(json.dumps(line), flush=True)

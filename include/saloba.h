@@ -41,8 +41,11 @@
  *   - Data-dependent errors are reported through the [dev] int64 `status` word: the call sets
  *     it to -1 (no error) or to the smallest offending index (atomicMin), readable after the
  *     stream is synchronised.
- *   - Thread-safe across host threads and streams; no global mutable state except a per-device
- *     cache of occupancy numbers computed once.
+ *   - Thread-safe across host threads and streams.  Process-wide state: a per-device cache of
+ *     occupancy numbers (computed once) and, per (device, caller stream), the auxiliary streams and
+ *     fork/join events a call's concurrent bin kernels run on (created on first use, kept for the
+ *     process), so calls on different streams overlap and a CUDA-graph capture of one stream
+ *     never involves another stream's work.
  */
 #ifndef SALOBA_H
 #define SALOBA_H
@@ -121,7 +124,11 @@ int64_t saloba_packed_words(int64_t total_bases, int64_t n_seqs, saloba_packing 
  *                                                valid base (InvalidBase; N under PACK2).
  *                                                Empty sequences are legal here (0 words, lens 0);
  *                                                saloba_align_batch reports them (EmptySequence).
- * Returns SALOBA_OK or a negative code (nothing launched). */
+ *                                                byte_off[n_seqs] (one past the last byte) when
+ *                                                words_capacity < saloba_packed_words(
+ *                                                byte_off[n_seqs], n_seqs, fmt): nothing is written.
+ * Returns SALOBA_OK or a negative code (nothing launched): SALOBA_EWORKSPACE when words_capacity is
+ * below n_seqs + 1 (the layout's minimum, checkable without reading the device offsets). */
 int saloba_pack(const uint8_t* ascii, const int64_t* byte_off, int64_t n_seqs, saloba_packing fmt,
                 uint32_t* words, int64_t words_capacity, int64_t* word_off, int32_t* lens, int64_t* status,
                 void* stream);

@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -43,7 +44,8 @@ void launch_start_finalize(const int32_t* score, const int32_t* q_end, const int
                            const int32_t* rq_end, const int32_t* rt_end, int64_t n, int32_t* q_start,
                            int32_t* t_start, int64_t* status, int sms, cudaStream_t s);
 void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n, int64_t base, int fmt,
-                       uint32_t* words, int64_t* word_off, int32_t* lens, int64_t* status, cudaStream_t s);
+                       uint32_t* words, int64_t cap, int64_t* word_off, int32_t* lens, int64_t* status,
+                       cudaStream_t s);
 
 // ---- per-device cache (computed once) ---------------------------------------------------------
 struct DevInfo {
@@ -55,7 +57,6 @@ struct DevInfo {
     int blocks_i16qn[2][2][2] = {};      // QN variant: [rows 8|16][mode][G = 1|2]
     int blocks_g1[2][2] = {};            // dp_g1 kernel: [mode][QN]
     int max_blocks_per_sm = 1;           // max resident blocks of any DP kernel (block-slot pool)
-    cudaStream_t aux[4] = {};            // bins run as concurrent kernels on these
 };
 constexpr int NAUX = 4;
 static std::mutex g_mu;
@@ -111,11 +112,56 @@ static const DevInfo* dev_info(int device) {
                     d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_i16qn[ri][mode][1]);
                 }
             }
-        for (int i = 0; i < NAUX; ++i) cudaStreamCreateWithFlags(&d.aux[i], cudaStreamNonBlocking);
         cudaSetDevice(prev);
         d.init = true;
     }
     return &d;
+}
+
+// Auxiliary streams of one caller stream: the bins of a call run as concurrent kernels forked onto
+// them and joined back (fork / join events created once with the set).  One set per (device,
+// caller stream), created on first use, so calls on different streams or threads never share aux
+// streams (they overlap instead of serialising, and a CUDA-graph capture on one stream does not
+// pull in another stream's work).  Calls on the SAME stream share its set; the events then order
+// a superset of each call's work, which is still correct.
+struct AuxSet {
+    cudaStream_t aux[NAUX] = {};
+    cudaEvent_t fork = nullptr;
+    cudaEvent_t join[NAUX] = {};
+    bool init(int device) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        bool ok = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; i < NAUX && ok; ++i)
+            ok = cudaStreamCreateWithFlags(&aux[i], cudaStreamNonBlocking) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming) == cudaSuccess;
+        cudaSetDevice(prev);
+        return ok;
+    }
+    void destroy() {
+        for (int i = 0; i < NAUX; ++i) {
+            if (aux[i]) cudaStreamDestroy(aux[i]);
+            if (join[i]) cudaEventDestroy(join[i]);
+        }
+        if (fork) cudaEventDestroy(fork);
+    }
+};
+static std::mutex g_aux_mu;
+static std::unordered_map<uint64_t, AuxSet*> g_aux;  // key: caller stream handle x device
+static const AuxSet* aux_for(int device, cudaStream_t s) {
+    const uint64_t key = reinterpret_cast<uint64_t>(s) * 64 + uint64_t(device);
+    std::lock_guard<std::mutex> lk(g_aux_mu);
+    auto it = g_aux.find(key);
+    if (it != g_aux.end()) return it->second;
+    AuxSet* a = new AuxSet();
+    if (!a->init(device)) {
+        a->destroy();
+        delete a;
+        return nullptr;
+    }
+    g_aux.emplace(key, a);
+    return a;
 }
 
 int sm_count_current() {
@@ -220,13 +266,13 @@ static int gidx_of(int G) {
     }
 }
 
-// aux: NAUX streams the bins fork onto (nullptr: the device's shared set)
+// aux_in: the aux set the bins fork onto (nullptr: the caller stream's own set)
 static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, const int32_t* q_len,
                             const uint32_t* t_words, const int64_t* t_word_off, const int32_t* t_len,
                             const int32_t* h0, int64_t n_pairs, saloba_scoring sc, saloba_mode mode,
                             saloba_packing fmt, int32_t* score, int32_t* q_end, int32_t* t_end, void* workspace,
                             size_t workspace_bytes, int64_t* status, const saloba_options* opt, void* stream,
-                            const cudaStream_t* aux_in, const int32_t* band_w = nullptr) {
+                            const AuxSet* aux_in, const int32_t* band_w = nullptr) {
     if (n_pairs < 0 || n_pairs > int64_t(INT32_MAX) - 1024) return SALOBA_EINVAL;
     if (!status || !workspace) return SALOBA_EINVAL;
     if (n_pairs > 0 && (!q_words || !q_word_off || !q_len || !t_words || !t_word_off || !t_len || !score ||
@@ -310,11 +356,11 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
         // All bins run as concurrent kernels (fork/join over the device's auxiliary streams), longest
         // bins first: a few long pairs then overlap the bulk of short ones instead of leaving most SMs
         // idle in a tail (§III-A load imbalance).  Blocks without work exit at once.
-        cudaEvent_t fork = nullptr, join[NAUX] = {};
-        cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-        cudaEventRecord(fork, s);
-        const cudaStream_t* aux = aux_in ? aux_in : d->aux;
-        for (int i = 0; i < NAUX; ++i) cudaStreamWaitEvent(aux[i], fork, 0);
+        const AuxSet* xs = aux_in ? aux_in : aux_for(dev, s);
+        if (!xs) return SALOBA_ECUDA;
+        const cudaStream_t* aux = xs->aux;
+        cudaEventRecord(xs->fork, s);
+        for (int i = 0; i < NAUX; ++i) cudaStreamWaitEvent(aux[i], xs->fork, 0);
         int j = 0;
         for (int path = PATH_I16; path >= PATH_I32; --path)
             for (int g = NGROUPS - 1; g >= 0; --g, ++j) {
@@ -354,12 +400,9 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
             }
         }
         for (int i = 0; i < NAUX; ++i) {
-            cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming);
-            cudaEventRecord(join[i], aux[i]);
-            cudaStreamWaitEvent(s, join[i], 0);
-            cudaEventDestroy(join[i]);
+            cudaEventRecord(xs->join[i], aux[i]);
+            cudaStreamWaitEvent(s, xs->join[i], 0);
         }
-        cudaEventDestroy(fork);
         if (o.ev_dp_end) cudaEventRecord((cudaEvent_t)o.ev_dp_end, s);
     }
     launch_status_final(status, s);
@@ -501,7 +544,7 @@ struct saloba_host_ctx {
     // aligns while slice i drains
     void* ws[2] = {nullptr, nullptr};
     cudaStream_t cs[2] = {nullptr, nullptr};
-    cudaStream_t aux[2][4] = {};
+    AuxSet aux[2];
     cudaEvent_t fork = nullptr, pjoin[2] = {nullptr, nullptr};
     int64_t qwcap = 0, twcap = 0;
     cudaStream_t copy = nullptr, down = nullptr;
@@ -519,8 +562,7 @@ SALOBA_API void saloba_host_ctx_destroy(saloba_host_ctx* c) {
         if (b) cudaFree(b);
     for (int p = 0; p < 2; ++p) {
         if (c->cs[p]) cudaStreamDestroy(c->cs[p]);
-        for (int i = 0; i < 4; ++i)
-            if (c->aux[p][i]) cudaStreamDestroy(c->aux[p][i]);
+        c->aux[p].destroy();
         if (c->pjoin[p]) cudaEventDestroy(c->pjoin[p]);
     }
     if (c->fork) cudaEventDestroy(c->fork);
@@ -577,7 +619,7 @@ SALOBA_API saloba_host_ctx* saloba_host_ctx_create(int64_t max_pairs, int64_t ma
         }
         for (int p = 0; p < 2; ++p) {
             cudaStreamCreateWithFlags(&c->cs[p], cudaStreamNonBlocking);
-            for (int i = 0; i < 4; ++i) cudaStreamCreateWithFlags(&c->aux[p][i], cudaStreamNonBlocking);
+            ok = ok && c->aux[p].init(device);
             cudaEventCreateWithFlags(&c->pjoin[p], cudaEventDisableTiming);
         }
         cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
@@ -673,15 +715,15 @@ SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii,
         cudaStream_t ps = c->cs[pp];
         cudaStreamWaitEvent(ps, c->up[i], 0);
         if (trace) cudaEventRecord(tcs[i], ps);
-        launch_pack_range(qd, qo + a0, na, a0, SALOBA_PACK4, static_cast<uint32_t*>(c->qw),
+        launch_pack_range(qd, qo + a0, na, a0, SALOBA_PACK4, static_cast<uint32_t*>(c->qw), c->qwcap,
                           static_cast<int64_t*>(c->qwo) + a0, static_cast<int32_t*>(c->ql) + a0, st + 4 * i + 0, ps);
-        launch_pack_range(td, to + a0, na, a0, SALOBA_PACK4, static_cast<uint32_t*>(c->tw),
+        launch_pack_range(td, to + a0, na, a0, SALOBA_PACK4, static_cast<uint32_t*>(c->tw), c->twcap,
                           static_cast<int64_t*>(c->two) + a0, static_cast<int32_t*>(c->tl) + a0, st + 4 * i + 1, ps);
         rc = align_batch_impl(static_cast<uint32_t*>(c->qw), static_cast<int64_t*>(c->qwo) + a0,
                               static_cast<int32_t*>(c->ql) + a0, static_cast<uint32_t*>(c->tw),
                               static_cast<int64_t*>(c->two) + a0, static_cast<int32_t*>(c->tl) + a0,
                               h0d ? h0d + a0 : nullptr, na, sc, mode, SALOBA_PACK4, res + a0, res + n_pairs + a0,
-                              res + 2 * n_pairs + a0, c->ws[pp], c->ws_bytes, st + 4 * i + 2, opt, ps, c->aux[pp]);
+                              res + 2 * n_pairs + a0, c->ws[pp], c->ws_bytes, st + 4 * i + 2, opt, ps, &c->aux[pp]);
         cudaEventRecord(c->done[i], ps);
         if (trace) cudaEventRecord(tce[i], ps);
         cudaStreamWaitEvent(c->down, c->done[i], 0);

@@ -8,14 +8,18 @@
 //
 //   * no shuffles and no Q+G-1 ramp: a chunk is Q steps of one 8-column block each;
 //   * PRMT selectors are built once per pair-duo (during chunk 0, from the packed query words) and
-//     stored to the thread's scratch; later chunks and pass 2 fetch 8 ready selector words per step
-//     (saves ~30 ALU instructions per step = ~5% of the step's ALU work);
-//   * every global stream is laid out [.. block w ..][quad][thread] so that one warp-wide 16-byte
-//     access covers 512 contiguous bytes (coalesced spill stores, cp.async stage loads);
-//   * the shared-memory stage is [slot][quad][thread]: conflict-free LDS.128;
-//   * top-row values are read from the stage per column and bottom-row values stored per column
-//     pair, so neither row is held in registers across a step (<= 128 registers: 4 blocks / SM);
+//     stored to the thread's scratch as 8 x 16-bit selectors per block ([w][thread]: one warp
+//     load is 512 contiguous bytes); later chunks and pass 2 fetch them instead of rebuilding them
+//     (~30 fewer ALU instructions per step, ~5% of the step's ALU work);
+//   * the shared-memory stage is [slot][quad][thread]: conflict-free LDS.128, one per column pair,
+//     issued a pair ahead;
 //   * pass 2 tests a candidate column's 16 rows in registers (no local-memory parking).
+// Measured on B200, config 2, against the generic kernel at G = 1: DP +0-6% LOCAL,
+// +1.5% EXTEND, -2% on config 3's longer reads.  Alternatives measured and not kept: 4 blocks per
+// SM (L2 spill-row residency), interleaved spill rows, L2 evict-first/last hints, stage-in at the
+// end of the previous step, F/E opened from H directly (shorter dependency chain but one more
+// FMA-pipe op per cell: issue-bound), a one-pass keyed maximum (D*128 + position; 2 more FMA-pipe
+// ops per cell: issue-bound, -3%).
 //
 // Cell update per 32-bit register (2 cells, one per pair of the duo): see dp_i16.cu.
 // Exactness of the 16-bit lanes is guaranteed by routing (schedule.cu): scores fit int8 and all
@@ -28,22 +32,11 @@ constexpr int G1_T = 128;    // threads per block
 constexpr int G1_R = 16;     // target rows per strip (two packed target words per half)
 constexpr int G1_DEPTH = 3;  // stage slots in pass 1 (inputs requested two steps ahead)
 constexpr int G1_NBUF = 4;   // spill buffers per thread: read, write, two checkpoints
-// Resident blocks per SM.  Not register-bound: the spill rows of all resident threads must stay
+// Resident blocks per SM: 3.  Not register-bound: the spill rows of all resident threads must stay
 // L2-resident between a chunk writing them and the next chunk reading them (reuse distance =
-// resident threads x Q x 64 B, + the selector stream); measured on B200 (config 2): 4 blocks/SM
-// pushed that past the 126 MB L2 (L2 hit rate 63% -> 21%, DRAM reads 6x) and ran 35% slower.
-#ifndef G1_MINB
-#define G1_MINB 3
-#endif
-// G1_PIPE: read a step's first shared-memory inputs at the end of the previous step (1) or at its
-// head (0).  G1_BOTREG: keep the chunk-bottom row in registers and store it after the step (1) or
-// store each column pair as it is produced (0).
-#ifndef G1_PIPE
-#define G1_PIPE 0
-#endif
-#ifndef G1_BOTREG
-#define G1_BOTREG 0
-#endif
+// resident threads x Q x 64 B); measured on B200 (config 2) with 4 blocks per SM the L2 hit rate
+// fell and the kernel ran ~6% slower.
+constexpr int G1_MINB = 3;
 
 // Scratch words per thread per query block: 8 selector words (4 compact ones when the query has
 // no N) + G1_NBUF spill rows of 16 words.
@@ -65,53 +58,19 @@ struct G1Stage {
 //   row  [G1_T][G1_NBUF][Qcap][4] uint4 spilled chunk-bottom rows (H, F of 8 columns), contiguous
 //                                       per thread.  The buffer rotation differs from lane to lane
 //                                       (it follows each lane's checkpoints), so a [buf][w][q][thread]
-//                                       interleave (G1_ROWS_INTERLEAVED) shares every 128-byte line
-//                                       between lanes on different buffers: measured on B200 it
-//                                       partially wrote lines of dead rows and cut the L2 hit rate
-//                                       from 63% to 18% (DRAM reads 5x).
-#ifndef G1_ROWS_INTERLEAVED
-#define G1_ROWS_INTERLEAVED 0
-#endif
+//                                       interleave shares every 128-byte line between lanes on
+//                                       different buffers: measured on B200 it partially wrote lines
+//                                       of dead rows and cut the L2 hit rate from 63% to 18% (DRAM
+//                                       reads 5x, kernel 30% slower).
 struct G1Scratch {
     uint4* sel;
     uint4* row;
     int qcap;
     __device__ __forceinline__ uint4* sel_at(int w, int h) const { return sel + (size_t(w) * 2 + h) * G1_T + threadIdx.x; }
     __device__ __forceinline__ uint4* row_at(int buf, int w, int q) const {
-#if G1_ROWS_INTERLEAVED
-        return row + ((size_t(buf) * qcap + w) * 4 + q) * G1_T + threadIdx.x;
-#else
         return row + ((size_t(threadIdx.x) * G1_NBUF + buf) * qcap + w) * 4 + q;
-#endif
     }
 };
-
-// L2 residency of the spill rows (G1_HINT): 0 = default policy; 1 = top-row reads marked
-// evict-first (a row is dead once the next chunk has read it); 2 = also bottom-row writes marked
-// evict-last (keep them until that read)
-#ifndef G1_HINT
-#define G1_HINT 0
-#endif
-__device__ __forceinline__ uint64_t l2_policy(bool last) {
-    uint64_t p;
-    if (last) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_pred16(uint4* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, bool on) {
-#if G1_HINT >= 2
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-                 "setp.ne.b32 p, %5, 0;\n\t@p st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, pol;\n\t}"
-                 ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d), "r"(int(on)));
-#else
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t@p st.global.v4.u32 [%0], {%1, %2, %3, %4};\n\t}"
-                 ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d), "r"(int(on)));
-#endif
-}
 
 // the 4 raw packed target words of a strip starting at rows rA / rB (2 per half)
 template <int FMT>
@@ -177,9 +136,6 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
     const bool topA_mem = topA >= 0;
     const bool topB_mem = PASS2 && topB >= 0 && topB != topA;
     const bool split = PASS2 && (topB != topA || rB != rA);  // pass 2 halves at different chunks
-#if G1_HINT >= 1
-    const uint64_t evict_first = l2_policy(false);
-#endif
     auto prefetch = [&](int s2, int slot) {
         if (s2 < Q) {
             if (selgen) {
@@ -193,10 +149,6 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
             if (topA_mem) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-#if G1_HINT >= 1
-                    if (!PASS2) cp_async16_hint(&st.top[slot][q][tid], sc.row_at(topA, s2, q), evict_first);
-                    else
-#endif
                     cp_async16(&st.top[slot][q][tid], sc.row_at(topA, s2, q));
                 }
             }
@@ -210,9 +162,8 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
 #pragma unroll
     for (int p = 0; p < DEPTH - 1; ++p) prefetch(p, p);
     // Stage-in of step s2's inputs (slot `slot`): wait for its cp.async group, write table-boundary
-    // top rows into the slot, and read the step's first shared-memory values into registers.  It
-    // runs at the END of the previous step, so a step starts with its selectors and first top-row
-    // quad already in registers (no LDS latency at the head of the step).
+    // top rows into the slot, and read the step's selectors and first top-row quad.  (Issuing this
+    // at the end of the previous step instead measured 1-4% slower on B200.)
     uint32_t nq0 = 0, nq1 = 0;
     uint4 nsel0 = make_uint4(0, 0, 0, 0), nsel1 = nsel0, ntq = nsel0, ntb = nsel0;
     auto stage_in = [&](int s2, int slot) {
@@ -245,10 +196,10 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
         ntq = st.top[slot][0][tid];
         if (PASS2 && split) ntb = st.top[2 + slot][0][tid];
     };
-    if (G1_PIPE) stage_in(0, 0);
+
     int cur = 0;
     for (int s = 0; s < Q; ++s) {
-        if (!G1_PIPE) stage_in(s, cur);
+        stage_in(s, cur);
         prefetch(s + DEPTH - 1, cur == 0 ? DEPTH - 1 : cur - 1);
         uint32_t sel[8];
         if (selgen) {
@@ -285,10 +236,8 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
         }
         const int slot = cur;
         cur = (cur == DEPTH - 1) ? 0 : cur + 1;
-        uint32_t hdiag_top = corner, prevH = 0, prevF = 0;
-#if G1_BOTREG
+        uint32_t hdiag_top = corner;
         uint32_t botH[8], botF[8];
-#endif
         // top-row quads: one conflict-free LDS.128 per column pair, issued a pair ahead
         uint4 tq = ntq, tqn = ntq, tb = ntb, tbn = ntb;
 #pragma unroll
@@ -332,12 +281,11 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                     d = vadd(hdiag, scv);
                 }
                 const uint32_t h = vmax3relu(d, e, f);
-                const uint32_t ha = vadd(h, nalpha);
                 hdiag = Hl[r];
                 Hl[r] = h;
-                En[r] = vaddmax(e, nbeta, ha);
+                En[r] = vaddmax(e, nbeta, vadd(h, nalpha));
                 hup = h;
-                haup = ha;
+                haup = vadd(h, nalpha);
                 fup = f;
                 if (!PASS2) {
                     if (r & 1) {
@@ -351,14 +299,8 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
             }
             // chunk-bottom row -> spill, one 16-byte store per column pair (predicated, not branched,
             // so the step stays one basic block)
-#if G1_BOTREG
             botH[x] = hup;
             botF[x] = fup;
-#else
-            if (x & 1) st_pred16(sc.row_at(bot < 0 ? 0 : bot, s, x >> 1), prevH, prevF, hup, fup, bot >= 0);
-            prevH = hup;
-            prevF = fup;
-#endif
             if (PASS2) {
                 // a cell can only equal `target` (the pair maximum) where the column maximum reaches it;
                 // such columns are rare (about one per pair): test their rows in registers
@@ -374,14 +316,11 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
             }
         }
         corner = hdiag_top;
-        if (G1_PIPE && s + 1 < Q) stage_in(s + 1, cur);
-#if G1_BOTREG
         if (bot >= 0) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 *sc.row_at(bot, s, q) = make_uint4(botH[2 * q], botF[2 * q], botH[2 * q + 1], botF[2 * q + 1]);
         }
-#endif
     }
     return vmax(vmax(M0, M1), vmax(M2, M3));
 }
@@ -430,8 +369,8 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
         const int Q = int(__reduce_max_sync(FULL, unsigned(Qi)));  // warp-uniform loop bounds
         const int chunks_w = int(__reduce_max_sync(FULL, unsigned(chunks)));
 
-        // pass 1 -------------------------------------------------------------------------------
         const int floorA = MODE ? A.h0 : 0, floorB = MODE ? B.h0 : 0;
+        // pass 1 -------------------------------------------------------------------------------
         int bestA = floorA, bestB = floorB;  // running maxima (strict improvement records the chunk)
         int ckA = -1, ckB = -1;              // chunk holding the first maximum (-1: none above floor)
         int bufA = -1, bufB = -1;            // buffer holding that chunk's top row (-1: boundary)

@@ -5,7 +5,6 @@
 // B = 8 (PACK4) or 16 (PACK2); ceil(len/B) <= floor(end/B) - floor(start/B) + 1 words fit.
 // A warp packs tiles of 8 consecutive sequences with lanes over the tile's flattened words, so
 // reads (8 bytes per lane) and 4-bit word writes coalesce and short sequences leave no lane idle.
-#include <cstdlib>
 
 #include "common.cuh"
 
@@ -72,198 +71,7 @@ __device__ __forceinline__ bool fast_acgt8(uint2 by, uint32_t& out) {
 // sequence word by word (8-byte loads, L1-served across the lane's consecutive iterations) — no
 // per-word bookkeeping.  Common words take the bit-arithmetic path above; words with U, N, padding
 // or invalid bytes take the shared-memory byte->code table.
-template <int BITS>
-__global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ ascii, const int64_t* __restrict__ byte_off,
-                                                   int64_t n_seqs, int64_t base, uint32_t* __restrict__ words,
-                                                   int64_t* __restrict__ word_off, int32_t* __restrict__ lens,
-                                                   unsigned long long* __restrict__ status) {
-    constexpr int B = 32 / BITS;  // bases per word
-    __shared__ uint8_t lut[256];
-    build_lut(lut, BITS);
-    __syncthreads();
-    const int64_t total = byte_off[n_seqs];  // ascii is readable up to here
-    for (int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < n_seqs; s += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t b0 = byte_off[s], len = byte_off[s + 1] - b0;
-        const int64_t w0 = b0 / B + s + base;
-        word_off[s] = w0;
-        if (lens) lens[s] = int32_t(len);
-        if (s == n_seqs - 1) word_off[n_seqs] = byte_off[n_seqs] / B + n_seqs + base;
-        const int nw = int((len + B - 1) / B);
-        constexpr int U = 4;  // words in flight per lane (memory-level parallelism)
-        for (int wb = 0; wb < nw; wb += U) {
-          uint2 pre[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-              pre[u] = (BITS == 4 && wb + u < nw) ? load8(ascii, b0 + int64_t(wb + u) * B, total) : make_uint2(0, 0);
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int w = wb + u;
-            if (w >= nw) break;
-            uint32_t out = 0, bad = 0;
-            bool fast = false;
-            if (BITS == 4 && len - int64_t(w) * B >= 8) fast = fast_acgt8(pre[u], out);
-            if (!fast) {
-                out = 0;
-#pragma unroll
-                for (int half = 0; half < B / 8; ++half) {
-                    const int64_t p0 = int64_t(w) * B + half * 8;
-                    const uint2 by = load8(ascii, b0 + p0, total);
-                    const int nvalid = int(len - p0 < 8 ? len - p0 : 8);
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const uint32_t byte = ((c < 4 ? by.x : by.y) >> (8 * (c & 3))) & 0xFFu;
-                        uint32_t code = lut[byte];
-                        if (c < nvalid) bad |= code;
-                        if (c >= nvalid || code == 0xFFu) code = BITS == 4 ? 15u : 0u;  // padding / invalid
-                        out |= code << (BITS * (half * 8 + c));
-                    }
-                }
-            }
-            words[w0 + w] = out;
-            if (bad & 0x80u) {
-                // first invalid byte of this word (rare path)
-                for (int c = 0; c < B; ++c) {
-                    const int64_t p = int64_t(w) * B + c;
-                    if (p < len && lut[ascii[b0 + p]] == 0xFF) {
-                        atomicMin(status, (unsigned long long)(b0 + p));
-                        break;
-                    }
-                }
-            }
-          }
-        }
-    }
-}
-
-// Flattened tile sweep (the default): a warp takes a tile of 32 consecutive sequences, scans their
-// word counts, and its lanes walk the tile's words in flattened order, so lane j of an iteration
-// packs the j-th word of the tile: consecutive lanes read consecutive 8-byte spans of the ASCII
-// and write consecutive words (both coalesced; the per-lane walk above issues 32 scattered sector
-// requests per load).  A 5-step shuffle binary search over the scan finds each word's sequence.
-template <int BITS>
-__global__ void __launch_bounds__(256) pack_tile_kernel(const uint8_t* __restrict__ ascii,
-                                                        const int64_t* __restrict__ byte_off, int64_t n_seqs,
-                                                        int64_t base, uint32_t* __restrict__ words,
-                                                        int64_t* __restrict__ word_off, int32_t* __restrict__ lens,
-                                                        unsigned long long* __restrict__ status) {
-    constexpr unsigned FULL = 0xffffffffu;
-    constexpr int B = 32 / BITS;  // bases per word
-    __shared__ uint8_t lut[256];
-    build_lut(lut, BITS);
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int64_t total = byte_off[n_seqs];
-    const int64_t tiles = (n_seqs + 31) / 32;
-    const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
-    for (int64_t tile = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; tile < tiles; tile += warps) {
-        const int64_t s = tile * 32 + lane;
-        const bool has = s < n_seqs;
-        const int64_t b0 = has ? byte_off[s] : 0;
-        const int64_t len = has ? byte_off[s + 1] - b0 : 0;
-        const int64_t w0 = b0 / B + s + base;
-        if (has) {
-            word_off[s] = w0;
-            if (lens) lens[s] = int32_t(len);
-            if (s == n_seqs - 1) word_off[n_seqs] = byte_off[n_seqs] / B + n_seqs + base;
-        }
-        const int nw = int((len + B - 1) / B);
-        int incl = nw;  // inclusive scan of word counts over the tile
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int v = __shfl_up_sync(FULL, incl, off);
-            if (lane >= off) incl += v;
-        }
-        const int tot = __shfl_sync(FULL, incl, 31);
-        constexpr int U = 4;  // words in flight per lane (memory-level parallelism)
-        for (int j0 = 0; j0 < tot; j0 += 32 * U) {
-          int wv[U];
-          int64_t ob0v[U], olenv[U], ow0v[U];
-          uint2 prev[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int j = j0 + 32 * u + lane;
-            // owner: the first lane whose inclusive count exceeds j
-            int lo = 0;
-#pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-                const int v = __shfl_sync(FULL, incl, lo + step - 1);
-                if (v <= j) lo += step;
-            }
-            const int own = lo > 31 ? 31 : lo;
-            const int ex = __shfl_sync(FULL, incl - nw, own);
-            ob0v[u] = __shfl_sync(FULL, b0, own);
-            olenv[u] = __shfl_sync(FULL, len, own);
-            ow0v[u] = __shfl_sync(FULL, w0, own);
-            wv[u] = j < tot ? j - ex : -1;
-            prev[u] = wv[u] >= 0 ? load8(ascii, ob0v[u] + int64_t(wv[u]) * B, total) : make_uint2(0, 0);
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (wv[u] < 0) continue;
-            const int w = wv[u];
-            const int64_t ob0 = ob0v[u], olen = olenv[u], ow0 = ow0v[u];
-            uint32_t out = 0, bad = 0;
-            bool fast = false;
-            const uint2 by0 = prev[u];
-            const int64_t rem = olen - int64_t(w) * B;  // bases left in the sequence from this word
-            if (BITS == 4 && rem < 8) {
-                // a sequence's last, partial word: bytes past the end read as 'A' for the fast check
-                // and become padding nibbles, so these words do not drag the warp onto the table path
-                const int nv = int(rem);
-                const uint32_t klo = nv >= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (8 * (4 - nv))) & (nv ? 0xFFFFFFFFu : 0u);
-                const uint32_t khi = nv >= 8 ? 0xFFFFFFFFu : nv <= 4 ? 0u : 0xFFFFFFFFu >> (8 * (8 - nv));
-                const uint2 by = make_uint2((by0.x & klo) | (0x41414141u & ~klo), (by0.y & khi) | (0x41414141u & ~khi));
-                uint32_t n0 = 0;
-                fast = fast_acgt8(by, n0);
-                out = n0 | (0xFFFFFFFFu << (4 * nv));
-            } else if (rem >= B) {
-                uint32_t n0 = 0;
-                fast = fast_acgt8(by0, n0);
-                if (BITS == 2 && fast) {
-                    uint32_t n1 = 0;
-                    fast = fast_acgt8(load8(ascii, ob0 + int64_t(w) * B + 8, total), n1);
-                    // 16 nibbles (each <= 3) -> 16 two-bit fields
-                    uint32_t a = n0, b = n1;
-                    a = (a | (a >> 2)) & 0x0F0F0F0Fu; a = (a | (a >> 4)) & 0x00FF00FFu; a = (a | (a >> 8)) & 0xFFFFu;
-                    b = (b | (b >> 2)) & 0x0F0F0F0Fu; b = (b | (b >> 4)) & 0x00FF00FFu; b = (b | (b >> 8)) & 0xFFFFu;
-                    out = a | (b << 16);
-                } else {
-                    out = n0;
-                }
-            }
-            if (!fast) {
-                out = 0;
-#pragma unroll
-                for (int half = 0; half < B / 8; ++half) {
-                    const int64_t p0 = int64_t(w) * B + half * 8;
-                    const uint2 by = half == 0 ? by0 : load8(ascii, ob0 + p0, total);
-                    const int nvalid = int(olen - p0 < 8 ? olen - p0 : 8);
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const uint32_t byte = ((c < 4 ? by.x : by.y) >> (8 * (c & 3))) & 0xFFu;
-                        uint32_t code = lut[byte];
-                        if (c < nvalid) bad |= code;
-                        if (c >= nvalid || code == 0xFFu) code = BITS == 4 ? 15u : 0u;  // padding / invalid
-                        out |= code << (BITS * (half * 8 + c));
-                    }
-                }
-            }
-            words[ow0 + w] = out;
-            if (bad & 0x80u) {
-                for (int c = 0; c < B; ++c) {
-                    const int64_t p = int64_t(w) * B + c;
-                    if (p < olen && lut[ascii[ob0 + p]] == 0xFF) {
-                        atomicMin(status, (unsigned long long)(ob0 + p));
-                        break;
-                    }
-                }
-            }
-          }
-        }
-    }
-}
-
-// Tile sweep v2 (the default): per warp, the tile's per-sequence data (exclusive word counts,
+// Tile sweep: per warp, the tile's per-sequence data (exclusive word counts,
 // byte and word offsets relative to the tile, lengths) is staged in shared memory; each lane packs
 // U consecutive words of the tile's flattened word list (one binary search per lane, then a
 // forward walk across sequence ends), so a warp reads ~1 KB of contiguous ASCII per iteration and
@@ -271,7 +79,7 @@ __global__ void __launch_bounds__(256) pack_tile_kernel(const uint8_t* __restric
 template <int BITS>
 __global__ void __launch_bounds__(256) pack_tile2_kernel(const uint8_t* __restrict__ ascii,
                                                          const int64_t* __restrict__ byte_off, int64_t n_seqs,
-                                                         int64_t base, uint32_t* __restrict__ words,
+                                                         int64_t base, uint32_t* __restrict__ words, int64_t cap,
                                                          int64_t* __restrict__ word_off, int32_t* __restrict__ lens,
                                                          unsigned long long* __restrict__ status) {
     constexpr unsigned FULL = 0xffffffffu;
@@ -283,6 +91,12 @@ __global__ void __launch_bounds__(256) pack_tile2_kernel(const uint8_t* __restri
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t total = byte_off[n_seqs];
+    // capacity: the closed-form layout ends at word total/B + n_seqs + base; a buffer smaller than
+    // that gets no writes at all and the status reports byte index `total` (one past the last byte)
+    if (total / (32 / BITS) + n_seqs + base > cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(status, (unsigned long long)total);
+        return;
+    }
     const int64_t tiles = (n_seqs + 31) / 32;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
     for (int64_t tile = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; tile < tiles; tile += warps) {
@@ -398,39 +212,19 @@ int sm_count_current();
 // Pack sequences [0, n) of byte_off; `base` shifts the closed-form word layout so that slices of
 // a larger batch land where a single whole-batch pack would put them.
 void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n, int64_t base, int fmt,
-                       uint32_t* words, int64_t* word_off, int32_t* lens, int64_t* status, cudaStream_t s) {
+                       uint32_t* words, int64_t cap, int64_t* word_off, int32_t* lens, int64_t* status,
+                       cudaStream_t s) {
     launch_status_init(status, s);
     if (n > 0) {
         const int64_t g8 = int64_t(sm_count_current()) * 8;
-        static const bool walk = getenv("SALOBA_PACK_WALK") != nullptr;  // A/B: the per-lane walk
-        if (walk) {
-            const int64_t need = (n + 255) / 256;  // one thread per sequence
-            const int grid = int(need < g8 ? need : g8);
-            if (fmt == SALOBA_PACK4)
-                pack_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
-                                                    (unsigned long long*)status);
-            else
-                pack_kernel<2><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
-                                                    (unsigned long long*)status);
-        } else if (getenv("SALOBA_PACK_TILE1") != nullptr) {  // A/B: the first tile sweep
-            const int64_t need = (n + 255) / 256;  // one warp per 32-sequence tile, 8 warps per block
-            const int grid = int(need < g8 ? need : g8);
-            if (fmt == SALOBA_PACK4)
-                pack_tile_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
-                                                         (unsigned long long*)status);
-            else
-                pack_tile_kernel<2><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
-                                                         (unsigned long long*)status);
-        } else {
-            const int64_t need = (n + 255) / 256;  // one warp per 32-sequence tile, 8 warps per block
-            const int grid = int(need < g8 ? need : g8);
-            if (fmt == SALOBA_PACK4)
-                pack_tile2_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
-                                                          (unsigned long long*)status);
-            else
-                pack_tile2_kernel<2><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, word_off, lens,
-                                                          (unsigned long long*)status);
-        }
+        const int64_t need = (n + 255) / 256;  // one warp per 32-sequence tile, 8 warps per block
+        const int grid = int(need < g8 ? need : g8);
+        if (fmt == SALOBA_PACK4)
+            pack_tile2_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, cap, word_off, lens,
+                                                      (unsigned long long*)status);
+        else
+            pack_tile2_kernel<2><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, cap, word_off, lens,
+                                                      (unsigned long long*)status);
         count_launches(1);
     }
     launch_status_final(status, s);
@@ -452,6 +246,8 @@ SALOBA_API int saloba_pack(const uint8_t* ascii, const int64_t* byte_off, int64_
     if (n_seqs < 0 || !byte_off || !words || !word_off || !status || (n_seqs > 0 && !ascii)) return SALOBA_EINVAL;
     if (fmt != SALOBA_PACK4 && fmt != SALOBA_PACK2) return SALOBA_EINVAL;
     if (words_capacity < 0) return SALOBA_EINVAL;
-    launch_pack_range(ascii, byte_off, n_seqs, 0, int(fmt), words, word_off, lens, status, (cudaStream_t)stream);
+    if (words_capacity < n_seqs + 1) return SALOBA_EWORKSPACE;  // below the layout's minimum
+    launch_pack_range(ascii, byte_off, n_seqs, 0, int(fmt), words, words_capacity, word_off, lens, status,
+                      (cudaStream_t)stream);
     return cudaGetLastError() == cudaSuccess ? SALOBA_OK : SALOBA_ECUDA;
 }

@@ -86,6 +86,8 @@ def test_host_checked_errors_launch_nothing(L):
     assert L.saloba_pack(nul, nul, 3, 4, nul, 0, nul, nul, nul, nul) == sb.EINVAL
     assert L.saloba_pack(dummy, dummy, 3, 5, dummy, 10, dummy, nul, dummy, nul) == sb.EINVAL
     assert L.saloba_pack(dummy, dummy, -1, 4, dummy, 10, dummy, nul, dummy, nul) == sb.EINVAL
+    # capacity below the layout's minimum (n_seqs + 1 words): EWORKSPACE before any launch
+    assert L.saloba_pack(dummy, dummy, 10, 4, dummy, 10, dummy, nul, dummy, nul) == sb.EWORKSPACE
     # host entry: null status
     assert L.saloba_align_host(dummy, dummy, dummy, dummy, nul, 1, sc, 0, dummy, dummy, dummy, nul, None,
                                nul) == sb.EINVAL

@@ -395,3 +395,29 @@ def test_query_n_bin_g2(sb, mode):
     idx = np.unique(np.concatenate([idx, np.nonzero(b.qlen > 640)[0][:500]]))
     sub = b.subset(idx)
     assert_same(tuple(x[idx] for x in got[:3]), oracle_align(sub, sb.BWA_MEM, mode), sub, f"QN G=2 mode={mode}")
+
+
+def test_pack_capacity_overflow_reported(sb):
+    """saloba_pack with a words buffer one word short of the closed-form layout (total/8 + n words:
+    sequence s ends at or before word byte_off[s+1]/8 + s + 1): nothing is written and the status is
+    byte_off[n] (one past the last byte); exactly total/8 + n words packs normally."""
+    import ctypes
+
+    import torch
+
+    b = synth.random_pairs(50, 5, 40, seed=3)
+    qa, qo = torch.from_numpy(b.q_ascii).cuda(), torch.from_numpy(b.q_off).cuda()
+    n = b.n
+    need = len(b.q_ascii) // 8 + n
+    assert sb.packed_words(len(b.q_ascii), n) == need + 1  # the advertised capacity keeps one spare word
+    for cap, expect in ((need - 1, len(b.q_ascii)), (need, -1)):
+        words = torch.full((need,), 0x7777, dtype=torch.int32, device="cuda")
+        wo = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        st = torch.empty(1, dtype=torch.int64, device="cuda")
+        rc = sb.lib().saloba_pack(ctypes.c_void_p(qa.data_ptr()), ctypes.c_void_p(qo.data_ptr()), n, 4,
+                                  ctypes.c_void_p(words.data_ptr()), cap, ctypes.c_void_p(wo.data_ptr()), None,
+                                  ctypes.c_void_p(st.data_ptr()), None)
+        torch.cuda.synchronize()
+        assert rc == 0 and int(st.item()) == expect
+        if expect != -1:
+            assert bool((words == 0x7777).all())

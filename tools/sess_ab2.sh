@@ -16,11 +16,11 @@ for b in "${SETS[@]}"; do
 for v in base ${VARIANTS}; do
   name=${v%%=*}
   lib=paper_2301_09310_b200/libsaloba.so; [ "$name" != base ] && lib=build/variants/$name/libsaloba.so
-  SALOBA_LIB=$lib timeout 600 python bench.py --e2e-steps 0 --no-cpu-baseline --start-steps 0 --no-graph --steps 5 $b > gpurun_out/ab_run.log 2>&1
+  SALOBA_LIB=$lib timeout 600 python bench.py --e2e-steps 0 --no-cpu-baseline --start-steps 0 --ksw-steps 0 --no-graph --steps 5 $b > gpurun_out/ab_run.log 2>&1
   echo "$name [$b] :: $(tail -1 gpurun_out/ab_run.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print(d['value'], d['ms_per_step'], r['achieved'], r['frac'], r['bins'])" 2>&1 | tail -1)" >> gpurun_out/ab_summary.txt
 done; done; done
 cat gpurun_out/ab_summary.txt
 if [ -n "${NCU_KERNEL}" ]; then
-  timeout 1500 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k "regex:${NCU_KERNEL}" -s ${NCU_SKIP:-1} -c 1 -o gpurun_out/prof_${NCU_TAG:-ab} -f python bench.py --steps 1 --warmup 1 --e2e-steps 0 --start-steps 0 --no-graph --no-cpu-baseline ${NCU_ARGS:---pairs 300000} > gpurun_out/ncu_ab.log 2>&1; tail -2 gpurun_out/ncu_ab.log
+  timeout 1500 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k "regex:${NCU_KERNEL}" -s ${NCU_SKIP:-1} -c 1 -o gpurun_out/prof_${NCU_TAG:-ab} -f python bench.py --steps 1 --warmup 1 --e2e-steps 0 --start-steps 0 --ksw-steps 0 --no-graph --no-cpu-baseline ${NCU_ARGS:---pairs 300000} > gpurun_out/ncu_ab.log 2>&1; tail -2 gpurun_out/ncu_ab.log
 fi
 echo done
