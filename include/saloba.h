@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define SALOBA_VERSION 1
+#define SALOBA_VERSION 2
 
 typedef struct {
     int32_t match;      /* >= 1        */
@@ -104,6 +104,14 @@ typedef struct {
     int32_t* long_group;  /* optional [dev] int32[1]: log2(G) the long bin ran with this call (4 or 5):
                              G=16 iff the bin holds >= 4 waves of G=16 subwarps (throughput), else
                              G=32 (half the per-pair latency: few long pairs finish sooner) */
+    unsigned long long* counters; /* optional [dev] uint64[8], ADDED to (SURVEY §8(f) NEXT-4 instrumentation
+                             of the int16x2 kernels, §IV-A / SPEC acceptance 3-5): [0] pass-1
+                             chunk passes of all work items (a work item = two pairs, one per 16-bit
+                             half); [1] their wavefront steps (Q + G - 1 per chunk pass, Q at G = 1);
+                             [2] spilled 64-byte blocks (the chunk-bottom H and F of 8 columns, both
+                             halves) written; [3] spilled blocks read back; [4] pass-2 chunk passes;
+                             [5] pass-2 steps; [6] pass-1 lane-strips (chunk passes x G); [7] work items.
+                             The counting costs one warp reduction + atomic per chunk; NULL: none */
     int32_t reserved[2];
 } saloba_options;
 

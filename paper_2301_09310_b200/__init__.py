@@ -58,7 +58,7 @@ class _Options(ctypes.Structure):
     _fields_ = [("force_group", ctypes.c_int32), ("force_path", ctypes.c_int32), ("keep_order", ctypes.c_int32),
                 ("i16_rows", ctypes.c_int32), ("ev_dp_begin", ctypes.c_void_p), ("ev_dp_end", ctypes.c_void_p),
                 ("bin_counts", ctypes.c_void_p), ("long_group", ctypes.c_void_p),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("counters", ctypes.c_void_p), ("reserved", ctypes.c_int32 * 2)]
 
 
 @dataclass(frozen=True)
@@ -113,6 +113,7 @@ class Options:
     bin_counts: torch.Tensor | None = None  # cuda int32[16] <- pairs per bin (path*8 + log2 G)
     i16_rows: int = 0  # 0 default (16); 8 = 8 target rows per lane in the int16x2 kernel
     long_group: torch.Tensor | None = None  # cuda int32[1] <- log2 G the long bin (13) ran with
+    counters: torch.Tensor | None = None  # cuda int64[8] += NEXT-4 counters (saloba.h saloba_options.counters)
 
     def _c(self) -> _Options:
         o = _Options(self.force_group, self.force_path, self.keep_order, self.i16_rows)
@@ -123,6 +124,8 @@ class Options:
             o.bin_counts = ctypes.c_void_p(self.bin_counts.data_ptr())
         if self.long_group is not None:
             o.long_group = ctypes.c_void_p(self.long_group.data_ptr())
+        if self.counters is not None:
+            o.counters = ctypes.c_void_p(self.counters.data_ptr())
         return o
 
 

@@ -350,6 +350,7 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
         a.long_gidx = long_gidx;
         a.band_w = band_w;
         a.i32_fast = i32_fast;
+        a.counters = o.counters;
         if (o.bin_counts) cudaMemcpyAsync(o.bin_counts, bin_count, NBINS * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
         if (o.long_group) cudaMemcpyAsync(o.long_group, long_gidx, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
         if (o.ev_dp_begin) cudaEventRecord((cudaEvent_t)o.ev_dp_begin, s);

@@ -119,7 +119,16 @@ struct AlignArgs {
     const int32_t* long_gidx; // group index that runs LONG_BIN (set by bin_scan_kernel); others exit
     const int32_t* band_w;    // NEXT-2: per-pair band half-width (cells |i-j| <= w), or nullptr
     int32_t i32_fast;         // 1: the call's scores fit int8 (FAST int32 kernels in bins 0..5)
+    unsigned long long* counters;  // NEXT-4 instrumentation (saloba_options.counters) or nullptr
 };
+
+// NEXT-4 counters: a warp-wide sum of each lane's contribution, one atomic per counter per warp
+__device__ __forceinline__ void count_warp(unsigned long long* ctr, int idx, unsigned long long v) {
+    unsigned long long t = v;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(ctr + idx, t);
+}
 
 // 8 consecutive bases [8w, 8w+8) of a packed sequence as 8 nibbles (base c in nibble c).
 // PACK4: one word.  PACK2: half of a word expanded to nibbles (no N, no padding code: the caller

@@ -418,6 +418,18 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
                                          st, sc, tw2);
         }
         __syncwarp(FULL);
+        if (a.counters) {  // NEXT-4 instrumentation (saloba_options.counters)
+            const bool it = A.p >= 0;
+            const bool p2 = __any_sync(FULL, need2);
+            count_warp(a.counters, 0, it ? chunks_w : 0);
+            count_warp(a.counters, 1, it ? uint64_t(chunks_w) * Q : 0);
+            count_warp(a.counters, 2, it ? uint64_t(chunks - 1) * Q : 0);
+            count_warp(a.counters, 3, it ? uint64_t(chunks_w - 1) * Q : 0);
+            count_warp(a.counters, 4, it && p2 ? 1 : 0);
+            count_warp(a.counters, 5, it && p2 ? Q : 0);
+            count_warp(a.counters, 6, it ? chunks_w : 0);
+            count_warp(a.counters, 7, it ? 1 : 0);
+        }
         if (A.p >= 0) {
             const int z = MODE ? -1 : 0;
             a.score[A.p] = bestA;

@@ -493,6 +493,18 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 * 128 / I16_THREADS : 
             }
         }
         __syncwarp(FULL);
+        if (a.counters) {  // NEXT-4 instrumentation: one contribution per work item (its lane k = 0)
+            const bool it = k == 0 && A.p >= 0;
+            const bool p2 = __any_sync(FULL, need2);
+            count_warp(a.counters, 0, it ? chunks_w : 0);
+            count_warp(a.counters, 1, it ? uint64_t(chunks_w) * (Q + G - 1) : 0);
+            count_warp(a.counters, 2, it ? uint64_t(chunks - 1) * Q : 0);
+            count_warp(a.counters, 3, it ? uint64_t(chunks_w - 1) * Q : 0);
+            count_warp(a.counters, 4, it && p2 ? 1 : 0);
+            count_warp(a.counters, 5, it && p2 ? Q + G - 1 : 0);
+            count_warp(a.counters, 6, it ? uint64_t(chunks_w) * G : 0);
+            count_warp(a.counters, 7, it ? 1 : 0);
+        }
         if (k == 0 && A.p >= 0) {
             const int z = MODE ? -1 : 0;
             a.score[A.p] = bestA;

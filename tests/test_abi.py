@@ -35,7 +35,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_version_and_strerror(L):
-    assert L.saloba_version() == 1
+    assert L.saloba_version() == 2
     for code in (0, -1, -2, -3, -4, 7):
         assert isinstance(L.saloba_strerror(code), bytes)
 
