@@ -44,6 +44,7 @@ def _lib():
         lib.oracle_ksw_extend.argtypes = ksw
         lib.oracle_ksw_table.argtypes = ksw + [p]
         lib.oracle_ksw_batch.argtypes = [p, p, p, p, p, i64, p, i32, p, p, i]
+        lib.oracle_traceback.argtypes = [p, i, p, i, i32, i32, i32, i32, i32, i32, i32, i32, p, i, p]
         _LIB = lib
     return _LIB
 
@@ -236,3 +237,31 @@ def ksw_batch(batch, flags=0, threads=None, **kw):
     _lib().oracle_ksw_batch(qa.ctypes.data, qo.ctypes.data, ta.ctypes.data, to.ctypes.data, h0.ctypes.data, n,
                             par.ctypes.data, flags, out.ctypes.data, st.ctypes.data, threads)
     return out[:, :n], st[:n]
+
+
+# ---- CIGAR traceback (oracle/traceback.c, reading 18) ------------
+CIGAR_OPS = "MID"
+
+
+def traceback(q, t, t_start, t_end, q_start, q_end, match=1, mismatch=-4, alpha=7, beta=1, cap=4096):
+    """(cigar string, global score of t[t_start..t_end] x q[q_start..q_end]) of one pair."""
+    q, t = _b(q), _b(t)
+    ops = (ctypes.c_uint32 * cap)()
+    out = (ctypes.c_int32 * 2)()
+    st = _lib().oracle_traceback(_buf(q), len(q), _buf(t), len(t), match, mismatch, alpha, beta, t_start, t_end,
+                                 q_start, q_end, ops, cap, out)
+    if st != OK:
+        raise ValueError(st)
+    return "".join(f"{ops[k] >> 4}{CIGAR_OPS[ops[k] & 15]}" for k in range(out[0])), int(out[1])
+
+
+def traceback_ops(q, t, t_start, t_end, q_start, q_end, match=1, mismatch=-4, alpha=7, beta=1, cap=4096):
+    """Raw BAM-encoded CIGAR elements ((len << 4) | op) of one pair, and the global score."""
+    q, t = _b(q), _b(t)
+    ops = (ctypes.c_uint32 * cap)()
+    out = (ctypes.c_int32 * 2)()
+    st = _lib().oracle_traceback(_buf(q), len(q), _buf(t), len(t), match, mismatch, alpha, beta, t_start, t_end,
+                                 q_start, q_end, ops, cap, out)
+    if st != OK:
+        raise ValueError(st)
+    return [int(ops[k]) for k in range(out[0])], int(out[1])
