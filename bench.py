@@ -407,27 +407,54 @@ def main():
 
         hb = synth.Batch(batch.q_ascii, pinned_copy(batch.q_off), batch.t_ascii, pinned_copy(batch.t_off),
                          pinned_copy(batch.h0))
-        out = torch.empty((3, n), dtype=torch.int32, pin_memory=True).numpy()
+        import ctypes
+
+        def timed(fn):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            te2 = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                if args.dist_backend != "nccl":
+                    te2 = te2.cpu()
+                dist.all_reduce(te2, op=dist.ReduceOp.MAX)
+            return total_cells * args.e2e_steps / (float(te2[0]) * 1e-3) / 1e9
+
+        # (a) the streaming API (saloba_stream_*): two host contexts in flight, batch k+1's upload and
+        # packing overlap batch k's alignment; every batch still uploads its ASCII and reads back its
+        # results inside the timed region
+        outs = [torch.empty((3, n), dtype=torch.int32, pin_memory=True).numpy() for _ in range(2)]
+        sts = [ctypes.c_int64(0), ctypes.c_int64(0)]
+        hs = sb.HostStream(n, len(batch.q_ascii), len(batch.t_ascii), max_q)
+        hs.submit(hb, outs[0], sts[0], sb.BWA_MEM, mode, opts)  # warm
+        hs.wait()
+
+        def stream_steps():
+            for k in range(args.e2e_steps):
+                hs.submit(hb, outs[k & 1], sts[k & 1], sb.BWA_MEM, mode, opts)
+            hs.wait()
+
+        e2e_val = timed(stream_steps)
+        assert sts[0].value == -1 and sts[1].value == -1
+        hs.close()
+        # (b) one synchronous call per batch (saloba_align_host_ctx, 4 pipelined slices inside a batch)
+        out = outs[0]
         hctx = sb.HostContext(n, len(batch.q_ascii), len(batch.t_ascii), max_q)
         sb.align_host(hb, sb.BWA_MEM, mode, opts, out=out, ctx=hctx)  # warm
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.e2e_steps):
-            _, _, _, hst = sb.align_host(hb, sb.BWA_MEM, mode, opts, out=out, ctx=hctx)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        te2 = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            if args.dist_backend != "nccl":
-                te2 = te2.cpu()
-            dist.all_reduce(te2, op=dist.ReduceOp.MAX)
-        e2e_val = total_cells * args.e2e_steps / (float(te2[0]) * 1e-3) / 1e9
+        e2e_sync = timed(lambda: [sb.align_host(hb, sb.BWA_MEM, mode, opts, out=out, ctx=hctx)
+                                  for _ in range(args.e2e_steps)])
+        hctx.close()
         h2d = int(len(batch.q_ascii) + len(batch.t_ascii) + 16 * (n + 1) + (4 * n if mode == sb.EXTEND else 0))
         e2e = {"value": round(e2e_val, 2), "unit": "GCUPS", "h2d_bytes_per_step": h2d * world,
-               "d2h_bytes_per_step": 12 * n * world, "api": "saloba_align_host_ctx (pinned host ASCII in, host results out, 4 pipelined slices of growing size)"}
+               "d2h_bytes_per_step": 12 * n * world,
+               "api": "saloba_stream_submit/_wait (pinned host ASCII in, host results out; two batches in flight)",
+               "sync_call_value": round(e2e_sync, 2),
+               "sync_call_api": "saloba_align_host_ctx (one blocking call per batch, 4 pipelined slices)"}
 
     # ---- optional: the same step captured once into a CUDA graph and replayed (launch-bound batches) ----
     graph = None

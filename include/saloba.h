@@ -28,7 +28,8 @@
  * Entry points: saloba_pack (A1); saloba_workspace_bytes + saloba_align_batch (A2-A4, device
  * buffers); saloba_align_host[_ctx] (A1-A4 from host buffers); saloba_partition (A5, shards for
  * the GPUs of one box); saloba_align_banded (banded DP);
- * saloba_locate_start (LOCAL start coordinates, NEXT-3); saloba_scatter_results (A5, rank 0
+ * saloba_locate_start (LOCAL start coordinates, NEXT-3); saloba_traceback (CIGAR, NEXT-3);
+ * saloba_scatter_results (A5, rank 0
  * puts gathered shards back in input order); saloba_ksw_extend (BWA-MEM-compatible extension,
  * NEXT-1); diagnostics at the end.
  *
@@ -222,6 +223,35 @@ int saloba_locate_start(const uint32_t* q_words, const int64_t* q_word_off, int6
                         const int32_t* t_end, int32_t* q_start, int32_t* t_start, void* workspace,
                         size_t workspace_bytes, int64_t* status, const saloba_options* opt, void* stream);
 
+/* ---- CIGAR traceback (LOCAL mode) ------------------------------------------ */
+
+/* Workspace for saloba_traceback: n_pairs pairs whose aligned regions span at most max_tlen target
+ * and max_qlen query bases (regions up to 256 rows and 32,768 cells in 16x16 tiles need no workspace
+ * beyond 512 B). */
+size_t saloba_traceback_workspace_bytes(int64_t n_pairs, int32_t max_qlen, int32_t max_tlen, int device);
+
+/* The CIGAR of each LOCAL result (reading 18; the paper reports score and end only,
+ * P:132-149): the global affine alignment of t[t_start..t_end] x q[q_start..q_end]
+ * under the same scheme (its optimum equals the local score), the optimal one whose op string read
+ * from the end is smallest with M < D < I (indels left-aligned).
+ *   q_words..t_word_off, fmt, sc  [dev] as for saloba_align_batch / saloba_locate_start
+ *   score, q_end, t_end           [dev] int32[n_pairs] forward LOCAL results
+ *   q_start, t_start              [dev] int32[n_pairs] from saloba_locate_start
+ *   max_qlen, max_tlen            bounds of the aligned region (q_end - q_start + 1 etc.)
+ *   cigar   [dev] uint32[n_pairs][cigar_cap]  output: BAM-encoded elements (length << 4 | op),
+ *                                             op M = 0, I = 1, D = 2, in forward order
+ *   n_ops   [dev] int32[n_pairs]   output: elements written; 0 when score == 0; -1 when score < 0
+ *                                  (a rejected pair) or the CIGAR does not fit cigar_cap
+ *   status  [dev] int64[1]  -1, or the smallest pair whose region's global score differs from
+ *                           `score` (inconsistent input), whose CIGAR overflowed, or whose region
+ *                           exceeds the workspace bounds
+ * Asynchronous on `stream`. */
+int saloba_traceback(const uint32_t* q_words, const int64_t* q_word_off, const uint32_t* t_words,
+                     const int64_t* t_word_off, int64_t n_pairs, saloba_scoring sc, saloba_packing fmt,
+                     const int32_t* score, const int32_t* q_start, const int32_t* q_end, const int32_t* t_start,
+                     const int32_t* t_end, int32_t max_qlen, int32_t max_tlen, uint32_t* cigar, int32_t cigar_cap,
+                     int32_t* n_ops, void* workspace, size_t workspace_bytes, int64_t* status, void* stream);
+
 /* ---- A5: length-balanced sharding over the GPUs of one box ------------------------ */
 
 /* Workspace (bytes) saloba_partition needs for n_pairs pairs (0 on a bad n_pairs). */
@@ -321,6 +351,25 @@ int saloba_align_host_ctx(saloba_host_ctx* ctx, const uint8_t* q_ascii, const in
                           const uint8_t* t_ascii, const int64_t* t_off, const int32_t* h0, int64_t n_pairs,
                           saloba_scoring sc, saloba_mode mode, int32_t* score, int32_t* q_end, int32_t* t_end,
                           int64_t* host_status, const saloba_options* opt, void* stream);
+
+/* Streaming host batches: two host contexts used alternately, so batch k+1's upload (and
+ * packing) overlaps batch k's alignment and download — steady-state throughput is bounded by the
+ * slower of the host-device link and the GPU, not by their sum.  Results of a batch are valid in
+ * its host buffers after a later submit on the same context (two calls later) or after
+ * saloba_stream_wait; *host_status is written then too.  Host buffers should be pinned and must
+ * stay untouched until then.  Not thread-safe: one host thread per stream context. */
+typedef struct saloba_stream_ctx saloba_stream_ctx;
+saloba_stream_ctx* saloba_stream_create(int64_t max_pairs, int64_t max_q_bytes, int64_t max_t_bytes,
+                                        int32_t max_qlen, int device);
+void saloba_stream_destroy(saloba_stream_ctx* sctx);
+/* Enqueue one batch (arguments as saloba_align_host_ctx, without a stream); blocks only to finish
+ * the batch submitted two calls earlier.  Returns that finish's code, or a host-checked error. */
+int saloba_stream_submit(saloba_stream_ctx* sctx, const uint8_t* q_ascii, const int64_t* q_off,
+                         const uint8_t* t_ascii, const int64_t* t_off, const int32_t* h0, int64_t n_pairs,
+                         saloba_scoring sc, saloba_mode mode, int32_t* score, int32_t* q_end, int32_t* t_end,
+                         int64_t* host_status, const saloba_options* opt);
+/* Wait for every submitted batch (their results and statuses are then valid). */
+int saloba_stream_wait(saloba_stream_ctx* sctx);
 
 /* Convenience: create a context sized for this batch, align, destroy. */
 int saloba_align_host(const uint8_t* q_ascii, const int64_t* q_off, const uint8_t* t_ascii, const int64_t* t_off,

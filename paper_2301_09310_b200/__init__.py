@@ -16,7 +16,7 @@ import torch
 __all__ = [
     "LOCAL", "EXTEND", "PACK4", "PACK2", "Scoring", "Options", "BWA_MEM", "SalobaError", "lib", "lib_path",
     "packed_words", "pack", "workspace_bytes", "align_batch", "align", "align_banded", "start_workspace_bytes", "locate_start", "partition", "scatter_results",
-    "KswParams", "BWA_KSW", "ksw_extend", "ksw_align", "KSW_FIELDS",
+    "KswParams", "BWA_KSW", "ksw_extend", "ksw_align", "KSW_FIELDS", "traceback", "cigar_strings",
     "align_host", "version", "EXPORTS",
 ]
 
@@ -28,8 +28,10 @@ OK, EINVAL, ECUDA, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4
 EXPORTS = ("saloba_packed_words", "saloba_pack", "saloba_workspace_bytes", "saloba_align_batch",
            "saloba_align_banded", "saloba_start_workspace_bytes", "saloba_locate_start",
            "saloba_partition_workspace_bytes", "saloba_partition", "saloba_scatter_results",
-           "saloba_ksw_workspace_bytes", "saloba_ksw_extend",
+           "saloba_ksw_workspace_bytes", "saloba_ksw_extend", "saloba_traceback_workspace_bytes",
+           "saloba_traceback",
            "saloba_host_ctx_create", "saloba_host_ctx_destroy", "saloba_align_host_ctx", "saloba_align_host",
+           "saloba_stream_create", "saloba_stream_destroy", "saloba_stream_submit", "saloba_stream_wait",
            "saloba_strerror", "saloba_version", "saloba_kernel_launches")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -159,6 +161,11 @@ def lib() -> ctypes.CDLL:
         L.saloba_ksw_extend.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, ctypes.POINTER(_KswParams), ctypes.c_int, i32,
                                         vp, vp, ctypes.c_size_t, vp, vp]
         L.saloba_ksw_extend.restype = ctypes.c_int
+        L.saloba_traceback_workspace_bytes.argtypes = [i64, i32, i32, ctypes.c_int]
+        L.saloba_traceback_workspace_bytes.restype = ctypes.c_size_t
+        L.saloba_traceback.argtypes = [vp, vp, vp, vp, i64, _Scoring, ctypes.c_int, vp, vp, vp, vp, vp, i32, i32, vp,
+                                       i32, vp, vp, ctypes.c_size_t, vp, vp]
+        L.saloba_traceback.restype = ctypes.c_int
         L.saloba_scatter_results.argtypes = [vp, vp, i64, i32, i64, vp, vp, vp, vp, vp]
         L.saloba_scatter_results.restype = ctypes.c_int
         L.saloba_start_workspace_bytes.argtypes = [i64, i64, i64, i32, ctypes.c_int]
@@ -175,6 +182,15 @@ def lib() -> ctypes.CDLL:
         L.saloba_host_ctx_destroy.restype = None
         L.saloba_align_host_ctx.argtypes = [vp] + list(L.saloba_align_host.argtypes)
         L.saloba_align_host_ctx.restype = ctypes.c_int
+        L.saloba_stream_create.argtypes = [i64, i64, i64, i32, ctypes.c_int]
+        L.saloba_stream_create.restype = vp
+        L.saloba_stream_destroy.argtypes = [vp]
+        L.saloba_stream_destroy.restype = None
+        L.saloba_stream_submit.argtypes = [vp, vp, vp, vp, vp, vp, i64, _Scoring, ctypes.c_int, vp, vp, vp, vp,
+                                           ctypes.POINTER(_Options)]
+        L.saloba_stream_submit.restype = ctypes.c_int
+        L.saloba_stream_wait.argtypes = [vp]
+        L.saloba_stream_wait.restype = ctypes.c_int
         L.saloba_strerror.argtypes = [ctypes.c_int]
         L.saloba_strerror.restype = ctypes.c_char_p
         L.saloba_version.restype = ctypes.c_int
@@ -375,6 +391,45 @@ def ksw_align(q_ascii, q_off, t_ascii, t_off, h0, params: KswParams = BWA_KSW, f
     return out, st, qst, tst
 
 
+def traceback(q_words, q_word_off, t_words, t_word_off, score, q_start, q_end, t_start, t_end,
+              scoring: Scoring = BWA_MEM, fmt: int = PACK4, cigar_cap: int = 64, max_qlen: int | None = None,
+              max_tlen: int | None = None, stream=None):
+    """CIGARs of LOCAL results (saloba_traceback): returns (cigar uint32[n, cap], n_ops int32[n], status)."""
+    n = score.numel()
+    dev = score.device
+    args = [_dev_tensor(x, d_, nm) for x, d_, nm in zip(
+        (q_words, q_word_off, t_words, t_word_off, score, q_start, q_end, t_start, t_end),
+        (torch.int32, torch.int64, torch.int32, torch.int64) + (torch.int32,) * 5,
+        ("q_words", "q_word_off", "t_words", "t_word_off", "score", "q_start", "q_end", "t_start", "t_end"))]
+    if max_qlen is None:
+        max_qlen = int((args[6] - args[5]).max().item()) + 1 if n > 0 else 1
+    if max_tlen is None:
+        max_tlen = int((args[8] - args[7]).max().item()) + 1 if n > 0 else 1
+    cigar = torch.empty((max(n, 1), cigar_cap), dtype=torch.int32, device=dev)
+    n_ops = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    ws = torch.empty(int(lib().saloba_traceback_workspace_bytes(n, max_qlen, max_tlen, dev.index)), dtype=torch.uint8,
+                     device=dev)
+    status = torch.empty(1, dtype=torch.int64, device=dev)
+    rc = lib().saloba_traceback(*[_p(x) for x in args[:4]], n, scoring._c(), fmt, *[_p(x) for x in args[4:]],
+                                max_qlen, max_tlen, _p(cigar), cigar_cap, _p(n_ops), _p(ws), ws.numel(), _p(status),
+                                _stream(stream))
+    _check(rc, "saloba_traceback")
+    return cigar[:n], n_ops[:n], status
+
+
+def cigar_strings(cigar, n_ops) -> list:
+    """Host-side formatting of saloba_traceback's output: CIGAR strings ("" for 0 ops, None for -1)."""
+    c = cigar.cpu().numpy().view("uint32")
+    k = n_ops.cpu().numpy()
+    out = []
+    for r in range(len(k)):
+        if k[r] < 0:
+            out.append(None)
+        else:
+            out.append("".join(f"{int(x) >> 4}{'MID'[int(x) & 15]}" for x in c[r, :k[r]]))
+    return out
+
+
 def start_workspace_bytes(n_pairs: int, q_words_total: int, t_words_total: int, max_qlen: int,
                           device: int | None = None) -> int:
     dev = torch.cuda.current_device() if device is None else device
@@ -531,6 +586,56 @@ class HostContext:
     def close(self):
         if self.handle:
             lib().saloba_host_ctx_destroy(ctypes.c_void_p(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class HostStream:
+    """Streaming host batches (saloba_stream_*): submit() enqueues a host batch and returns at once
+    (it only finishes the batch submitted two calls earlier), so a batch's upload overlaps the
+    previous batch's alignment.  Results land in the given host arrays (pinned: numpy views of
+    torch pin_memory tensors) and are valid after wait() or two submits later."""
+
+    def __init__(self, max_pairs: int, max_q_bytes: int, max_t_bytes: int, max_qlen: int, device=None):
+        dev = torch.cuda.current_device() if device is None else device
+        self.handle = lib().saloba_stream_create(max_pairs, max_q_bytes, max_t_bytes, max_qlen, dev)
+        if not self.handle:
+            raise SalobaError(ECUDA, "saloba_stream_create")
+        self._keep = []  # host arrays of the batches in flight (kept alive until finished)
+
+    def submit(self, batch, out, status, scoring: Scoring = BWA_MEM, mode: int = LOCAL,
+               options: Options | None = None):
+        """out: int32 host array (3, n) (score, q_end, t_end); status: ctypes.c_int64 receiving -1 or
+        the first bad pair once the batch is finished."""
+        import numpy as np
+
+        n = len(batch.q_off) - 1
+        qo = np.ascontiguousarray(batch.q_off, np.int64)
+        to = np.ascontiguousarray(batch.t_off, np.int64)
+        h0 = np.ascontiguousarray(batch.h0, np.int32) if mode == EXTEND else None
+        o = out if isinstance(out, np.ndarray) else out.numpy()
+        opt = ctypes.byref(options._c()) if options is not None else None
+        keep = (batch.q_ascii, batch.t_ascii, qo, to, h0, o)
+        self._keep = (self._keep + [keep])[-2:]
+        rc = lib().saloba_stream_submit(
+            ctypes.c_void_p(self.handle), ctypes.c_void_p(batch.q_ascii.ctypes.data), ctypes.c_void_p(qo.ctypes.data),
+            ctypes.c_void_p(batch.t_ascii.ctypes.data), ctypes.c_void_p(to.ctypes.data),
+            ctypes.c_void_p(h0.ctypes.data) if h0 is not None else None, n, scoring._c(), mode,
+            ctypes.c_void_p(o[0].ctypes.data), ctypes.c_void_p(o[1].ctypes.data), ctypes.c_void_p(o[2].ctypes.data),
+            ctypes.byref(status), opt)
+        _check(rc, "saloba_stream_submit")
+
+    def wait(self):
+        _check(lib().saloba_stream_wait(ctypes.c_void_p(self.handle)), "saloba_stream_wait")
+
+    def close(self):
+        if self.handle:
+            lib().saloba_stream_destroy(ctypes.c_void_p(self.handle))
             self.handle = None
 
     def __del__(self):

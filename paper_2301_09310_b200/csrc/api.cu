@@ -27,17 +27,13 @@ void launch_dp_i16(int mode, int gidx, int grid, const AlignArgs& a, int bin, cu
 const void* dp_i16_kernel_ptr(int mode, int gidx, int fmt, int rows);
 const void* dp_i16_qn_kernel_ptr(int mode, int rows, int gidx);
 void launch_dp_i16_qn(int mode, int gidx, int grid, const AlignArgs& a, cudaStream_t s);
-const void* dp_g1_kernel_ptr(int mode, int fmt, bool qn);
+const void* dp_g1_kernel_ptr(int mode, int fmt, bool qn, bool band);
 int g1_threads();
 int64_t g1_scratch_words(int64_t qcap);
 void launch_dp_g1(int mode, int grid, const AlignArgs& a, int bin, bool qn, cudaStream_t s);
-// the G = 1 int16x2 bins run the dedicated kernel of dp_g1.cu (16-row strips); 8-row strips
-// (Options.i16_rows = 8) and builds with SALOBA_G1_LEGACY keep the generic dp_i16 kernel
-#ifdef SALOBA_G1_LEGACY
-static bool use_g1(int) { return false; }
-#else
+// the G = 1 int16x2 bins run the dedicated kernel of dp_g1.cu (16-row strips, banded variant);
+// 8-row strips (Options.i16_rows = 8, an A/B knob) keep the generic dp_i16 kernel
 static bool use_g1(int rows) { return rows != 8; }
-#endif
 void launch_reverse_prefix(int fmt, const uint32_t* words, const int64_t* word_off, const int32_t* end,
                            const int32_t* score, int64_t n, uint32_t* out, int32_t* out_len, int sms, cudaStream_t s);
 void launch_start_finalize(const int32_t* score, const int32_t* q_end, const int32_t* t_end, const int32_t* rscore,
@@ -98,8 +94,12 @@ static const DevInfo* dev_info(int device) {
         for (int mode = 0; mode < 2; ++mode)
             for (int qn = 0; qn < 2; ++qn) {
                 int nb = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_g1_kernel_ptr(mode, SALOBA_PACK4, qn != 0),
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_g1_kernel_ptr(mode, SALOBA_PACK4, qn != 0, false),
                                                               g1_threads(), 0);
+                int nbb = 0;  // the banded variant (NEXT-2): the grid takes the smaller occupancy
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, dp_g1_kernel_ptr(mode, SALOBA_PACK4, false, true),
+                                                              g1_threads(), 0);
+                if (nbb > 0) nb = std::min(nb, nbb);
                 d.blocks_g1[mode][qn] = std::max(1, nb);
                 d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_g1[mode][qn]);
             }
@@ -328,7 +328,7 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
             while (min_gidx < NGROUPS - 1 && duos * (int64_t(1) << min_gidx) < lanes) ++min_gidx;
     }
     ClassifyArgs ca{q_words, q_word_off, int(fmt), sc.match, q_len, t_len, h0, n_pairs, int(mode), force_g,
-                    band_w ? 1 : o.force_path, o.keep_order, i16_rows, Qsup * 8, score, q_end, t_end, kv.keys_in,
+                    o.force_path, o.keep_order, i16_rows, Qsup * 8, score, q_end, t_end, kv.keys_in,
                     kv.vals_in, bin_count, (unsigned long long*)status, long_qmax, band_w, i32_fast, min_gidx};
     const int64_t cap16 = int64_t(grid_for(d, int(mode), PATH_I16, NGROUPS - 2, i16_rows)) * (I16_THREADS / 16) * 2;
     if (run_classify_sort(ca, kv, bin_start, d->sms, long_gidx, cap16, s) != cudaSuccess) return SALOBA_ECUDA;
@@ -387,7 +387,8 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
             launch_dp_i32(int(mode), NGROUPS - 1, grid_for(d, int(mode), PATH_I32, NGROUPS - 1), a, I32_WIDE_BIN,
                           aux[(j + 1) % NAUX]);
         }
-        if (fmt == SALOBA_PACK4) {  // QN bins: int16x2 G=1 / G=2 pairs whose query contains N
+        if (fmt == SALOBA_PACK4 && !band_w) {  // QN bins: int16x2 G=1 / G=2 pairs whose query contains N
+                                               // (query-N pairs of banded calls run int32)
             for (int g = 0; g <= 1; ++g) {
                 if (g == 0 && use_g1(i16_rows)) {
                     AlignArgs a1 = a;
@@ -551,6 +552,16 @@ struct saloba_host_ctx {
     cudaStream_t copy = nullptr, down = nullptr;
     cudaEvent_t up[HOST_SLICES], done[HOST_SLICES];
     int64_t* hst = nullptr;  // pinned status readback
+    // the batch enqueued last and not yet finished (saloba_stream_*: several contexts in flight)
+    struct Pending {
+        bool active = false;
+        int nsl = 0, rc = SALOBA_OK;
+        int64_t cut[HOST_SLICES + 1] = {};
+        const int64_t *q_off = nullptr, *t_off = nullptr;
+        int64_t qb0 = 0, tb0 = 0, n_pairs = 0;
+        cudaStream_t s = nullptr;
+        int64_t* host_status = nullptr;
+    } pend;
 };
 
 SALOBA_API void saloba_host_ctx_destroy(saloba_host_ctx* c) {
@@ -645,10 +656,13 @@ int64_t pair_of_byte(const int64_t* off, int64_t n, int64_t byte) {  // k with o
 }
 }  // namespace
 
-SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii, const int64_t* q_off,
-                                     const uint8_t* t_ascii, const int64_t* t_off, const int32_t* h0, int64_t n_pairs,
-                                     saloba_scoring sc, saloba_mode mode, int32_t* score, int32_t* q_end,
-                                     int32_t* t_end, int64_t* host_status, const saloba_options* opt, void* stream) {
+// Enqueue one host batch on a context (no host synchronisation); host_finish() waits for it and
+// fills *host_status.  saloba_align_host_ctx = enqueue + finish; saloba_stream_* keeps two contexts
+// in flight so one batch's upload overlaps the previous batch's compute.
+static int host_enqueue(saloba_host_ctx* c, const uint8_t* q_ascii, const int64_t* q_off, const uint8_t* t_ascii,
+                        const int64_t* t_off, const int32_t* h0, int64_t n_pairs, saloba_scoring sc,
+                        saloba_mode mode, int32_t* score, int32_t* q_end, int32_t* t_end, int64_t* host_status,
+                        const saloba_options* opt, void* stream, bool allow_trace) {
     if (!c || n_pairs < 0 || !q_off || !t_off || !host_status) return SALOBA_EINVAL;
     if (n_pairs > 0 && (!q_ascii || !t_ascii || !score || !q_end || !t_end)) return SALOBA_EINVAL;
     if (mode == SALOBA_EXTEND && n_pairs > 0 && !h0) return SALOBA_EINVAL;
@@ -737,9 +751,7 @@ SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii,
         cudaEventRecord(c->pjoin[p], c->cs[p]);
         cudaStreamWaitEvent(s, c->pjoin[p], 0);
     }
-    cudaStreamSynchronize(c->copy);
-    const cudaError_t e = cudaStreamSynchronize(c->down);
-    if (trace) {
+    if (trace && allow_trace) {
         cudaStreamSynchronize(s);
         for (int i = 0; i < nsl; ++i) {
             float u = 0, cs = 0, ce = 0;
@@ -747,24 +759,137 @@ SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii,
             cudaEventElapsedTime(&cs, tr0, tcs[i]);
             cudaEventElapsedTime(&ce, tr0, tce[i]);
             fprintf(stderr, "[saloba trace] slice %d: upload done %.3f ms, compute %.3f -> %.3f ms\n", i, u, cs, ce);
+        }
+    }
+    if (trace) {
+        for (int i = 0; i < nsl; ++i) {
             cudaEventDestroy(tup[i]);
             cudaEventDestroy(tcs[i]);
             cudaEventDestroy(tce[i]);
         }
         cudaEventDestroy(tr0);
     }
-    cudaStreamSynchronize(s);
     cudaSetDevice(prev);
-    if (rc != SALOBA_OK) return rc;
+    auto& P = c->pend;
+    P.active = true;
+    P.nsl = nsl;
+    P.rc = rc;
+    for (int i = 0; i <= nsl; ++i) P.cut[i] = cut[i];
+    P.q_off = q_off;
+    P.t_off = t_off;
+    P.qb0 = qb0;
+    P.tb0 = tb0;
+    P.n_pairs = n_pairs;
+    P.s = s;
+    P.host_status = host_status;
+    return rc;
+}
+
+static int host_finish(saloba_host_ctx* c) {
+    auto& P = c->pend;
+    if (!P.active) return SALOBA_OK;
+    P.active = false;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->copy);
+    const cudaError_t e = cudaStreamSynchronize(c->down);
+    cudaStreamSynchronize(P.s);
+    cudaSetDevice(prev);
+    if (P.rc != SALOBA_OK) return P.rc;
     if (e != cudaSuccess) return SALOBA_ECUDA;
     int64_t bad = INT64_MAX;
-    for (int i = 0; i < nsl; ++i) {
-        if (c->hst[4 * i + 0] >= 0) bad = std::min(bad, pair_of_byte(q_off, n_pairs, c->hst[4 * i + 0] + qb0));
-        if (c->hst[4 * i + 1] >= 0) bad = std::min(bad, pair_of_byte(t_off, n_pairs, c->hst[4 * i + 1] + tb0));
-        if (c->hst[4 * i + 2] >= 0) bad = std::min(bad, cut[i] + c->hst[4 * i + 2]);
+    for (int i = 0; i < P.nsl; ++i) {
+        if (c->hst[4 * i + 0] >= 0) bad = std::min(bad, pair_of_byte(P.q_off, P.n_pairs, c->hst[4 * i + 0] + P.qb0));
+        if (c->hst[4 * i + 1] >= 0) bad = std::min(bad, pair_of_byte(P.t_off, P.n_pairs, c->hst[4 * i + 1] + P.tb0));
+        if (c->hst[4 * i + 2] >= 0) bad = std::min(bad, P.cut[i] + c->hst[4 * i + 2]);
     }
-    *host_status = bad == INT64_MAX ? -1 : bad;
+    *P.host_status = bad == INT64_MAX ? -1 : bad;
     return SALOBA_OK;
+}
+
+SALOBA_API int saloba_align_host_ctx(saloba_host_ctx* c, const uint8_t* q_ascii, const int64_t* q_off,
+                                     const uint8_t* t_ascii, const int64_t* t_off, const int32_t* h0, int64_t n_pairs,
+                                     saloba_scoring sc, saloba_mode mode, int32_t* score, int32_t* q_end,
+                                     int32_t* t_end, int64_t* host_status, const saloba_options* opt, void* stream) {
+    if (!c) return SALOBA_EINVAL;
+    const int rf = host_finish(c);  // a batch left in flight by the streaming API
+    if (rf != SALOBA_OK) return rf;
+    const int rc = host_enqueue(c, q_ascii, q_off, t_ascii, t_off, h0, n_pairs, sc, mode, score, q_end, t_end,
+                                host_status, opt, stream, true);
+    if (rc != SALOBA_OK) {
+        c->pend.active = false;
+        return rc;
+    }
+    return host_finish(c);
+}
+
+// ---- streaming host batches (two host contexts in flight) -------------------------------------
+struct saloba_stream_ctx {
+    saloba_host_ctx* h[2] = {nullptr, nullptr};
+    cudaStream_t s[2] = {nullptr, nullptr};  // private caller streams (the legacy stream would serialise)
+    int64_t submitted = 0;
+    int device = 0;
+};
+
+SALOBA_API void saloba_stream_destroy(saloba_stream_ctx* x) {
+    if (!x) return;
+    for (int i = 0; i < 2; ++i) {
+        if (x->h[i]) {
+            host_finish(x->h[i]);
+            saloba_host_ctx_destroy(x->h[i]);
+        }
+        if (x->s[i]) cudaStreamDestroy(x->s[i]);
+    }
+    delete x;
+}
+
+SALOBA_API saloba_stream_ctx* saloba_stream_create(int64_t max_pairs, int64_t max_q_bytes, int64_t max_t_bytes,
+                                                   int32_t max_qlen, int device) {
+    saloba_stream_ctx* x = new saloba_stream_ctx();
+    x->device = device;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    bool ok = cudaSetDevice(device) == cudaSuccess;
+    for (int i = 0; i < 2 && ok; ++i) {
+        x->h[i] = saloba_host_ctx_create(max_pairs, max_q_bytes, max_t_bytes, max_qlen, device);
+        ok = x->h[i] != nullptr && cudaStreamCreateWithFlags(&x->s[i], cudaStreamNonBlocking) == cudaSuccess;
+    }
+    cudaSetDevice(prev);
+    if (!ok) {
+        saloba_stream_destroy(x);
+        return nullptr;
+    }
+    return x;
+}
+
+SALOBA_API int saloba_stream_submit(saloba_stream_ctx* x, const uint8_t* q_ascii, const int64_t* q_off,
+                                    const uint8_t* t_ascii, const int64_t* t_off, const int32_t* h0, int64_t n_pairs,
+                                    saloba_scoring sc, saloba_mode mode, int32_t* score, int32_t* q_end,
+                                    int32_t* t_end, int64_t* host_status, const saloba_options* opt) {
+    if (!x || !host_status) return SALOBA_EINVAL;
+    const int slot = int(x->submitted & 1);
+    saloba_host_ctx* c = x->h[slot];
+    const int rf = host_finish(c);  // the batch submitted two calls ago on this context
+    if (rf != SALOBA_OK) return rf;
+    const int rc = host_enqueue(c, q_ascii, q_off, t_ascii, t_off, h0, n_pairs, sc, mode, score, q_end, t_end,
+                                host_status, opt, x->s[slot], false);
+    if (rc != SALOBA_OK) {
+        c->pend.active = false;
+        return rc;
+    }
+    ++x->submitted;
+    return SALOBA_OK;
+}
+
+SALOBA_API int saloba_stream_wait(saloba_stream_ctx* x) {
+    if (!x) return SALOBA_EINVAL;
+    int rc = SALOBA_OK;
+    for (int k = 0; k < 2; ++k) {  // the older batch first
+        const int r = host_finish(x->h[int((x->submitted + k) & 1)]);
+        if (r != SALOBA_OK && rc == SALOBA_OK) rc = r;
+    }
+    return rc;
 }
 
 SALOBA_API int saloba_align_host(const uint8_t* q_ascii, const int64_t* q_off, const uint8_t* t_ascii,

@@ -24,6 +24,8 @@
 // Cell update per 32-bit register (2 cells, one per pair of the duo): see dp_i16.cu.
 // Exactness of the 16-bit lanes is guaranteed by routing (schedule.cu): scores fit int8 and all
 // H, E, F stay inside int16 (SURVEY §8(c) reading 8).
+#include <type_traits>
+
 #include "dp_i16_common.cuh"
 
 namespace saloba {
@@ -84,6 +86,16 @@ __device__ __forceinline__ void g1_target_raw(const HalfInfo& A, const HalfInfo&
     }
 }
 
+// NEXT-2 banded DP (reading 16) on this kernel: the step range of a strip, the spill-row
+// index bases and the band half-widths (both halves).  Without a band: [0, Q-1], bases 0.
+struct G1Band {
+    int s_begin, s_first, s_end;  // steps [s_begin, s_end]; s_begin = s_first - 1 is a corner visit
+    int rbaseA, rbaseB;           // index base of the spill row read (per half: pass 2 may split)
+    int hiA, hiB;                 // last block the strip above computed; its top row beyond is 0
+    int wbase;                    // index base of the spill row written
+    uint32_t wpk, nwpk;           // pack2(wA, wB), pack2(-wA, -wB)
+};
+
 // One 16-row strip of both halves.
 //   PASS2 = false: returns the lane's maximum of the diagonal candidates D over the strip (max H =
 //     max(0, max D): a positive H reached through a gap is strictly below an earlier cell).
@@ -91,13 +103,18 @@ __device__ __forceinline__ void g1_target_raw(const HalfInfo& A, const HalfInfo&
 //   selgen: build the selectors from the query words and store them (chunk 0 of pass 1).
 //   topA / topB: spill buffer of the top row per half (-1: the table boundary); bot: buffer that
 //     receives the bottom row (-1: none).
-template <int MODE, int FMT, bool PASS2, bool QN>
+//   BAND: only cells |i - j| <= w (per half) are in the table; the strip runs steps
+//     [bd.s_begin, bd.s_end] (a corner visit + the union of the warp's band blocks), blocks that
+//     cross a band edge mask their out-of-band cells to H = E = F = 0, selectors are built every
+//     step (no selector scratch), and spill rows are indexed relative to the writing strip's first
+//     step so a row needs ~(2w + 16)/8 + 3 blocks whatever the query length.
+template <int MODE, int FMT, bool PASS2, bool QN, bool BAND = false>
 __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, const HalfInfo& A, const HalfInfo& B,
                                              const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
                                              const int rA, const int rB, const int topA, const int topB,
                                              const int bot, const bool selgen, const uint32_t target,
                                              int (&hit)[4], G1Stage& st, const G1Scratch& sc,
-                                             const uint32_t (&twraw)[4]) {
+                                             const uint32_t (&twraw)[4], const G1Band& bd) {
     const int tid = threadIdx.x;
     const int al = a.alpha, be = a.beta;
     const uint32_t nbeta = pack2(-be, -be), nalpha = pack2(-al, -al), noGap = pack2(-al - be, -al - be);
@@ -136,8 +153,9 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
     const bool topA_mem = topA >= 0;
     const bool topB_mem = PASS2 && topB >= 0 && topB != topA;
     const bool split = PASS2 && (topB != topA || rB != rA);  // pass 2 halves at different chunks
+    const int s_last = BAND ? bd.s_end : Q - 1;
     auto prefetch = [&](int s2, int slot) {
-        if (s2 < Q) {
+        if (s2 <= s_last) {
             if (selgen) {
                 const int wi = FMT == SALOBA_PACK2 ? (s2 >> 1) : s2;
                 if (8 * s2 < A.n) cp_async4(&st.q[slot][0][tid], qwA + wi);
@@ -146,21 +164,22 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                 cp_async16(&st.sel[slot][0][tid], sc.sel_at(s2, 0));
                 if (QN) cp_async16(&st.sel[slot][1][tid], sc.sel_at(s2, 1));
             }
-            if (topA_mem) {
+            if (topA_mem && (!BAND || s2 <= bd.hiA)) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    cp_async16(&st.top[slot][q][tid], sc.row_at(topA, s2, q));
-                }
+                for (int q = 0; q < 4; ++q)
+                    cp_async16(&st.top[slot][q][tid], sc.row_at(topA, BAND ? s2 - bd.rbaseA : s2, q));
             }
-            if (topB_mem) {
+            if (topB_mem && (!BAND || s2 <= bd.hiB)) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) cp_async16(&st.top[2 + slot][q][tid], sc.row_at(topB, s2, q));
+                for (int q = 0; q < 4; ++q)
+                    cp_async16(&st.top[2 + slot][q][tid], sc.row_at(topB, BAND ? s2 - bd.rbaseB : s2, q));
             }
         }
         cp_async_commit();
     };
+    const int s0 = BAND ? bd.s_begin : 0;
 #pragma unroll
-    for (int p = 0; p < DEPTH - 1; ++p) prefetch(p, p);
+    for (int p = 0; p < DEPTH - 1; ++p) prefetch(s0 + p, p);
     // Stage-in of step s2's inputs (slot `slot`): wait for its cp.async group, write table-boundary
     // top rows into the slot, and read the step's selectors and first top-row quad.  (Issuing this
     // at the end of the previous step instead measured 1-4% slower on B200.)
@@ -186,6 +205,16 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                                                       pack2(0, MODE ? max(0, B.h0 - al - be * (j + 1)) : 0), noGap);
             }
         }
+        if (BAND) {  // top-row blocks the strip above never computed are out of band: H = F = 0
+            if (topA_mem && s2 > bd.hiA) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) st.top[slot][q][tid] = make_uint4(0, 0, 0, 0);
+            }
+            if (PASS2 && split && topB_mem && s2 > bd.hiB) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) st.top[2 + slot][q][tid] = make_uint4(0, 0, 0, 0);
+            }
+        }
         if (selgen) {
             nq0 = st.q[slot][0][tid];
             nq1 = st.q[slot][1][tid];
@@ -198,9 +227,35 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
     };
 
     int cur = 0;
-    for (int s = 0; s < Q; ++s) {
+    for (int s = s0; s <= s_last; ++s) {
         stage_in(s, cur);
         prefetch(s + DEPTH - 1, cur == 0 ? DEPTH - 1 : cur - 1);
+        if (BAND && s < bd.s_first) {
+            // corner visit of the block left of the band: nothing computed; the corner of the first
+            // band block is this block's top-row H at its last column, and the column left of the
+            // band is out of band for every row of the strip (H = E = 0)
+            const uint4 t3 = st.top[cur][3][tid];
+            corner = t3.z;
+            if (PASS2 && split) corner = prmt(corner, st.top[2 + cur][3][tid].z, 0x7610);
+#pragma unroll
+            for (int r = 0; r < G1_R; ++r) {
+                Hl[r] = 0;
+                En[r] = nbeta;  // E(i, first band column) = max(0 - alpha, 0 - beta)
+            }
+            cur = (cur == DEPTH - 1) ? 0 : cur + 1;
+            continue;
+        }
+        // BAND: does this block cross a band edge of either half (warp-uniform: then every lane masks)
+        bool edge = false;
+        uint32_t dpk = 0;
+        if (BAND) {
+            const int wA = int(bd.wpk & 0xFFFFu), wB = int(bd.wpk >> 16);
+            const bool inA = rA + 15 - 8 * s <= wA && 8 * s + 7 - rA <= wA;
+            const bool inB = rB + 15 - 8 * s <= wB && 8 * s + 7 - rB <= wB;
+            edge = __any_sync(0xffffffffu, !(inA && inB));
+            // i - j at (r, x) = (r0 - 8s) + (r - x), clamped far outside any band (int16 halves)
+            dpk = pack2(min(max(rA - 8 * s, -16000), 16000), min(max(rB - 8 * s, -16000), 16000));
+        }
         uint32_t sel[8];
         if (selgen) {
             const uint32_t qcA = staged_codes<FMT>(nq0, s, A.n);
@@ -217,7 +272,9 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                     sel[x] = (sel[x] & 0xFFFFu) | (((zA >> (4 * x + 3)) & 1u) * 0x00FF0000u) |
                              (((zB >> (4 * x + 3)) & 1u) * 0xFF000000u);
             }
-            if (QN) {
+            if (BAND) {
+                // banded strips build selectors every step (no selector scratch)
+            } else if (QN) {
                 *sc.sel_at(s, 0) = make_uint4(sel[0], sel[1], sel[2], sel[3]);
                 *sc.sel_at(s, 1) = make_uint4(sel[4], sel[5], sel[6], sel[7]);
             } else {  // compact: two 16-bit selectors per word (PRMT reads only the low 16 bits)
@@ -236,96 +293,188 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
         }
         const int slot = cur;
         cur = (cur == DEPTH - 1) ? 0 : cur + 1;
-        uint32_t hdiag_top = corner;
+        // the step body: 8 columns x 16 rows fully unrolled, one straight-line block
         uint32_t botH[8], botF[8];
-        // top-row quads: one conflict-free LDS.128 per column pair, issued a pair ahead
-        uint4 tq = ntq, tqn = ntq, tb = ntb, tbn = ntb;
-#pragma unroll
-        for (int x = 0; x < 8; ++x) {
-            uint32_t hup, fup;
-            {
-                if (!(x & 1)) {
-                    tq = tqn;
-                    if (PASS2 && split) tb = tbn;
-                    if (x + 2 < 8) {
-                        tqn = st.top[slot][(x >> 1) + 1][tid];
-                        if (PASS2 && split) tbn = st.top[2 + slot][(x >> 1) + 1][tid];
+        auto step_body = [&](auto) {
+            uint32_t hdiag_top = corner;
+            // top-row quads: one conflict-free LDS.128 per column pair, issued a pair ahead
+            uint4 tq = ntq, tqn = ntq, tb = ntb, tbn = ntb;
+    #pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                uint32_t hup, fup;
+                {
+                    if (!(x & 1)) {
+                        tq = tqn;
+                        if (PASS2 && split) tb = tbn;
+                        if (x + 2 < 8) {
+                            tqn = st.top[slot][(x >> 1) + 1][tid];
+                            if (PASS2 && split) tbn = st.top[2 + slot][(x >> 1) + 1][tid];
+                        }
+                    }
+                    hup = (x & 1) ? tq.z : tq.x;
+                    fup = (x & 1) ? tq.w : tq.y;
+                    if (PASS2 && split) {  // high halves from half B's own checkpoint row
+                        hup = prmt(hup, (x & 1) ? tb.z : tb.x, 0x7610);
+                        fup = prmt(fup, (x & 1) ? tb.w : tb.y, 0x7610);
                     }
                 }
-                hup = (x & 1) ? tq.z : tq.x;
-                fup = (x & 1) ? tq.w : tq.y;
-                if (PASS2 && split) {  // high halves from half B's own checkpoint row
-                    hup = prmt(hup, (x & 1) ? tb.z : tb.x, 0x7610);
-                    fup = prmt(fup, (x & 1) ? tb.w : tb.y, 0x7610);
-                }
-            }
-            uint32_t haup = vadd(hup, nalpha);
-            uint32_t hdiag = hdiag_top;
-            hdiag_top = hup;
-            uint32_t nm = 0;
-            if constexpr (QN) nm = prmt(sel[x], 0u, 0x3322);  // 0xFFFF per half whose column is N
-            uint32_t dprev = 0;
-#pragma unroll
-            for (int r = 0; r < G1_R; ++r) {
-                const uint32_t f = vaddmax(fup, nbeta, haup);
-                const uint32_t e = En[r];
-                uint32_t scv = prmt(tabA[r], tabB[r], sel[x]);
-                if constexpr (QN) scv = (scv & ~nm) | (mmw & nm);
-                uint32_t d;
-                if (MODE) {
-                    // dead-zero (EXTEND): D = hdiag + s if hdiag > 0, else <= 0, as
-                    // min(hdiag + s, lambda * hdiag) with lambda = 2^k >= match + 1 (one IMAD
-                    // scales both halves: hdiag >= 0 and lambda * hdiag <= 32767 by routing)
-                    d = vaddmin(hdiag, scv, hdiag * lam);
-                } else {
-                    d = vadd(hdiag, scv);
-                }
-                const uint32_t h = vmax3relu(d, e, f);
-                hdiag = Hl[r];
-                Hl[r] = h;
-                En[r] = vaddmax(e, nbeta, vadd(h, nalpha));
-                hup = h;
-                haup = vadd(h, nalpha);
-                fup = f;
-                if (!PASS2) {
-                    if (r & 1) {
-                        if ((r & 7) == 1) M0 = vmax3(M0, dprev, d);
-                        if ((r & 7) == 3) M1 = vmax3(M1, dprev, d);
-                        if ((r & 7) == 5) M2 = vmax3(M2, dprev, d);
-                        if ((r & 7) == 7) M3 = vmax3(M3, dprev, d);
+                uint32_t haup = vadd(hup, nalpha);
+                uint32_t hdiag = hdiag_top;
+                hdiag_top = hup;
+                uint32_t nm = 0;
+                if constexpr (QN) nm = prmt(sel[x], 0u, 0x3322);  // 0xFFFF per half whose column is N
+                uint32_t dprev = 0;
+    #pragma unroll
+                for (int r = 0; r < G1_R; ++r) {
+                    const uint32_t f = vaddmax(fup, nbeta, haup);
+                    const uint32_t e = En[r];
+                    uint32_t scv = prmt(tabA[r], tabB[r], sel[x]);
+                    if constexpr (QN) scv = (scv & ~nm) | (mmw & nm);
+                    uint32_t d;
+                    if (MODE) {
+                        // dead-zero (EXTEND): D = hdiag + s if hdiag > 0, else <= 0, as
+                        // min(hdiag + s, lambda * hdiag) with lambda = 2^k >= match + 1 (one IMAD
+                        // scales both halves: hdiag >= 0 and lambda * hdiag <= 32767 by routing)
+                        d = vaddmin(hdiag, scv, hdiag * lam);
+                    } else {
+                        d = vadd(hdiag, scv);
                     }
-                    dprev = d;
+                    const uint32_t h = vmax3relu(d, e, f);
+                    hdiag = Hl[r];
+                    Hl[r] = h;
+                    En[r] = vaddmax(e, nbeta, vadd(h, nalpha));
+                    hup = h;
+                    haup = vadd(h, nalpha);
+                    fup = f;
+                    if (!PASS2) {
+                        if (r & 1) {
+                            if ((r & 7) == 1) M0 = vmax3(M0, dprev, d);
+                            if ((r & 7) == 3) M1 = vmax3(M1, dprev, d);
+                            if ((r & 7) == 5) M2 = vmax3(M2, dprev, d);
+                            if ((r & 7) == 7) M3 = vmax3(M3, dprev, d);
+                        }
+                        dprev = d;
+                    }
+                }
+                // chunk-bottom row -> spill, one 16-byte store per column pair (predicated, not branched,
+                // so the step stays one basic block)
+                botH[x] = hup;
+                botF[x] = fup;
+                if (PASS2) {
+                    // a cell can only equal `target` (the pair maximum) where the column maximum reaches it;
+                    // such columns are rare (about one per pair): test their rows in registers
+                    uint32_t cm = vmax3(vmax3(Hl[0], Hl[1], Hl[2]), vmax3(Hl[3], Hl[4], Hl[5]), vmax3(Hl[6], Hl[7], Hl[8]));
+                    cm = vmax3(cm, vmax3(Hl[9], Hl[10], Hl[11]), vmax3(Hl[12], Hl[13], Hl[14]));
+                    cm = vmax(cm, Hl[15]);
+                    if (lo16(cm) >= lo16(target) || hi16(cm) >= hi16(target)) {
+                        uint32_t bits = 0;
+    #pragma unroll
+                        for (int r = 0; r < G1_R; ++r) bits |= eq_bits(Hl[r], target, r);
+                        take_hit(bits, 8 * s + x, rA, rB, hit);
+                    }
                 }
             }
-            // chunk-bottom row -> spill, one 16-byte store per column pair (predicated, not branched,
-            // so the step stays one basic block)
-            botH[x] = hup;
-            botF[x] = fup;
-            if (PASS2) {
-                // a cell can only equal `target` (the pair maximum) where the column maximum reaches it;
-                // such columns are rare (about one per pair): test their rows in registers
-                uint32_t cm = vmax3(vmax3(Hl[0], Hl[1], Hl[2]), vmax3(Hl[3], Hl[4], Hl[5]), vmax3(Hl[6], Hl[7], Hl[8]));
-                cm = vmax3(cm, vmax3(Hl[9], Hl[10], Hl[11]), vmax3(Hl[12], Hl[13], Hl[14]));
-                cm = vmax(cm, Hl[15]);
-                if (lo16(cm) >= lo16(target) || hi16(cm) >= hi16(target)) {
-                    uint32_t bits = 0;
+            corner = hdiag_top;
+        };
+        // Band-edge steps take a compact variant (columns in a rolled loop): a second fully unrolled
+        // body made the step code too large for the instruction cache (ncu: 44% no-instruction stalls)
+        auto edge_body = [&]() {
+            uint32_t hdiag_top = corner;
+#pragma unroll 1
+            for (int x = 0; x < 8; ++x) {
+                const uint4 tqx = st.top[slot][x >> 1][tid];
+                uint32_t hup = (x & 1) ? tqx.z : tqx.x, fup = (x & 1) ? tqx.w : tqx.y;
+                if (PASS2 && split) {
+                    const uint4 tbx = st.top[2 + slot][x >> 1][tid];
+                    hup = prmt(hup, (x & 1) ? tbx.z : tbx.x, 0x7610);
+                    fup = prmt(fup, (x & 1) ? tbx.w : tbx.y, 0x7610);
+                }
+                uint32_t selx = sel[0];
 #pragma unroll
-                    for (int r = 0; r < G1_R; ++r) bits |= eq_bits(Hl[r], target, r);
-                    take_hit(bits, 8 * s + x, rA, rB, hit);
+                for (int k = 1; k < 8; ++k) selx = x == k ? sel[k] : selx;
+                uint32_t haup = vadd(hup, nalpha);
+                uint32_t hdiag = hdiag_top;
+                hdiag_top = hup;
+                const uint32_t tx = vadd(dpk, pack2(-x, -x));
+                uint32_t dprev = 0;
+#pragma unroll
+                for (int r = 0; r < G1_R; ++r) {
+                    const uint32_t f = vaddmax(fup, nbeta, haup);
+                    const uint32_t e = En[r];
+                    const uint32_t scv = prmt(tabA[r], tabB[r], selx);
+                    uint32_t d = MODE ? vaddmin(hdiag, scv, hdiag * lam) : vadd(hdiag, scv);
+                    uint32_t h = vmax3relu(d, e, f);
+                    const uint32_t t = vadd(tx, pack2(r, r));
+                    const uint32_t mk = __vcmples2(t, bd.wpk) & __vcmpges2(t, bd.nwpk);
+                    h &= mk;
+                    d &= mk;
+                    hdiag = Hl[r];
+                    Hl[r] = h;
+                    En[r] = vaddmax(e & mk, nbeta, vadd(h, nalpha));
+                    hup = h;
+                    haup = vadd(h, nalpha);
+                    fup = f & mk;
+                    if (!PASS2) {
+                        if (r & 1) {
+                            if ((r & 7) == 1) M0 = vmax3(M0, dprev, d);
+                            if ((r & 7) == 3) M1 = vmax3(M1, dprev, d);
+                            if ((r & 7) == 5) M2 = vmax3(M2, dprev, d);
+                            if ((r & 7) == 7) M3 = vmax3(M3, dprev, d);
+                        }
+                        dprev = d;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (x == k) {
+                        botH[k] = hup;
+                        botF[k] = fup;
+                    }
+                }
+                if (PASS2) {
+                    uint32_t cm = vmax3(vmax3(Hl[0], Hl[1], Hl[2]), vmax3(Hl[3], Hl[4], Hl[5]), vmax3(Hl[6], Hl[7], Hl[8]));
+                    cm = vmax3(cm, vmax3(Hl[9], Hl[10], Hl[11]), vmax3(Hl[12], Hl[13], Hl[14]));
+                    cm = vmax(cm, Hl[15]);
+                    if (lo16(cm) >= lo16(target) || hi16(cm) >= hi16(target)) {
+                        uint32_t bits = 0;
+#pragma unroll
+                        for (int r = 0; r < G1_R; ++r) bits |= eq_bits(Hl[r], target, r);
+                        take_hit(bits, 8 * s + x, rA, rB, hit);
+                    }
                 }
             }
-        }
-        corner = hdiag_top;
+            corner = hdiag_top;
+        };
+        if (BAND && edge) edge_body();
+        else step_body(std::false_type{});
         if (bot >= 0) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                *sc.row_at(bot, s, q) = make_uint4(botH[2 * q], botF[2 * q], botH[2 * q + 1], botF[2 * q + 1]);
+                *sc.row_at(bot, BAND ? s - bd.wbase : s, q) =
+                    make_uint4(botH[2 * q], botF[2 * q], botH[2 * q + 1], botF[2 * q + 1]);
         }
     }
     return vmax(vmax(M0, M1), vmax(M2, M3));
 }
 
-template <int MODE, int FMT, bool QN>
+// warp-uniform band step range of a strip starting at row r0 (both halves, union over the warp);
+// a half without rows in the strip, or a dummy half, contributes nothing
+__device__ __forceinline__ void g1_band_range(int rA, int rB, const HalfInfo& A, const HalfInfo& B, int wA, int wB,
+                                              int& lo, int& hi) {
+    int l = INT_MAX, h = -1;
+    if (A.p >= 0 && rA < A.m) {
+        l = max(0, rA - wA) >> 3;
+        h = min(((A.n + 7) >> 3) - 1, (rA + 15 + wA) >> 3);
+    }
+    if (B.p >= 0 && rB < B.m) {
+        l = min(l, max(0, rB - wB) >> 3);
+        h = max(h, min(((B.n + 7) >> 3) - 1, (rB + 15 + wB) >> 3));
+    }
+    lo = int(__reduce_min_sync(0xffffffffu, unsigned(l)));
+    hi = int(__reduce_max_sync(0xffffffffu, unsigned(h + 1))) - 1;
+}
+
+template <int MODE, int FMT, bool QN, bool BAND>
 __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int bin) {
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -370,6 +519,12 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
         const int chunks_w = int(__reduce_max_sync(FULL, unsigned(chunks)));
 
         const int floorA = MODE ? A.h0 : 0, floorB = MODE ? B.h0 : 0;
+        // NEXT-2 band half-widths (clamped: a band past the table is the whole table)
+        const int wA = BAND && A.p >= 0 ? min(a.band_w[A.p], 32000) : 32000;
+        const int wB = BAND && B.p >= 0 ? min(a.band_w[B.p], 32000) : 32000;
+        G1Band bd{0, 0, Q - 1, 0, 0, Q, Q, 0, pack2(wA, wB), pack2(-wA, -wB)};
+        int prev_base = 0, prev_hi = -1;     // BAND: the strip above's spill base and last block
+        int ckbA = 0, ckbB = 0, ckhA = -1, ckhB = -1;  // BAND: base / last block of each checkpoint
         // pass 1 -------------------------------------------------------------------------------
         int bestA = floorA, bestB = floorB;  // running maxima (strict improvement records the chunk)
         int ckA = -1, ckB = -1;              // chunk holding the first maximum (-1: none above floor)
@@ -384,19 +539,43 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
             if (c + 1 < chunks_w) g1_target_raw<FMT>(A, B, twA, twB, (c + 1) * G1_R, (c + 1) * G1_R, twn);
             const bool last = (c + 1 >= chunks);
             int dummy[4];
-            const uint32_t m = g1_strip<MODE, FMT, false, QN>(a, Q, A, B, qwA, qwB, c * G1_R, c * G1_R, rd, rd,
-                                                              last ? -1 : wr, c == 0, 0u, dummy, st, sc, twc);
+            uint32_t m = 0;
+            int hi_now = -1;
+            bool run = true;
+            if (BAND) {
+                int lo, hi;
+                g1_band_range(c * G1_R, c * G1_R, A, B, wA, wB, lo, hi);
+                run = lo <= hi;
+                bd.s_first = lo;
+                bd.s_begin = max(0, lo - 1);
+                bd.s_end = hi;
+                bd.wbase = bd.s_begin;
+                bd.rbaseA = bd.rbaseB = prev_base;
+                bd.hiA = bd.hiB = prev_hi;
+                hi_now = run ? hi : -1;
+            }
+            if (run)
+                m = g1_strip<MODE, FMT, false, QN, BAND>(a, Q, A, B, qwA, qwB, c * G1_R, c * G1_R, rd, rd,
+                                                         last ? -1 : wr, BAND || c == 0, 0u, dummy, st, sc, twc, bd);
             if (c < chunks) {
                 if (lo16(m) > bestA) {
                     bestA = lo16(m);
                     ckA = c;
                     bufA = rd;
+                    ckbA = prev_base;
+                    ckhA = prev_hi;
                 }
                 if (hi16(m) > bestB) {
                     bestB = hi16(m);
                     ckB = c;
                     bufB = rd;
+                    ckbB = prev_base;
+                    ckhB = prev_hi;
                 }
+            }
+            if (BAND) {
+                prev_base = bd.wbase;
+                prev_hi = hi_now;
             }
             if (!last) {
                 rd = wr;
@@ -414,8 +593,20 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
             const uint32_t target = pack2(ckA >= 0 ? bestA : 0x7FFF, ckB >= 0 ? bestB : 0x7FFF);
             uint32_t tw2[4];
             g1_target_raw<FMT>(A, B, twA, twB, cA * G1_R, cB * G1_R, tw2);
-            g1_strip<MODE, FMT, true, QN>(a, Q, A, B, qwA, qwB, cA * G1_R, cB * G1_R, bA, bB, -1, false, target, hit,
-                                         st, sc, tw2);
+            if (BAND) {
+                int lo, hi;
+                g1_band_range(cA * G1_R, cB * G1_R, A, B, wA, wB, lo, hi);
+                bd.s_first = lo;
+                bd.s_begin = max(0, lo - 1);
+                bd.s_end = hi;
+                bd.rbaseA = ckA >= 0 ? ckbA : ckbB;
+                bd.hiA = ckA >= 0 ? ckhA : ckhB;
+                bd.rbaseB = ckB >= 0 ? ckbB : bd.rbaseA;
+                bd.hiB = ckB >= 0 ? ckhB : bd.hiA;
+            }
+            if (!BAND || bd.s_first <= bd.s_end)
+                g1_strip<MODE, FMT, true, QN, BAND>(a, Q, A, B, qwA, qwB, cA * G1_R, cB * G1_R, bA, bB, -1, BAND, target,
+                                                    hit, st, sc, tw2, bd);
         }
         __syncwarp(FULL);
         if (a.counters) {  // NEXT-4 instrumentation (saloba_options.counters)
@@ -445,20 +636,22 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
     release_block_slot(a.slot_bitmap, bslot);
 }
 
-template <int MODE>
+template <int MODE, bool BAND>
 static const void* g1_ptr(int fmt, bool qn) {
-    if (qn) return (const void*)dp_g1_kernel<MODE, SALOBA_PACK4, true>;
-    return fmt == SALOBA_PACK2 ? (const void*)dp_g1_kernel<MODE, SALOBA_PACK2, false>
-                               : (const void*)dp_g1_kernel<MODE, SALOBA_PACK4, false>;
+    if (qn && !BAND) return (const void*)dp_g1_kernel<MODE, SALOBA_PACK4, true, false>;
+    return fmt == SALOBA_PACK2 ? (const void*)dp_g1_kernel<MODE, SALOBA_PACK2, false, BAND>
+                               : (const void*)dp_g1_kernel<MODE, SALOBA_PACK4, false, BAND>;
 }
-const void* dp_g1_kernel_ptr(int mode, int fmt, bool qn) {
-    return mode == SALOBA_EXTEND ? g1_ptr<1>(fmt, qn) : g1_ptr<0>(fmt, qn);
+// banded calls (NEXT-2) run the BAND variant; query-N pairs of banded calls take the int32 path
+const void* dp_g1_kernel_ptr(int mode, int fmt, bool qn, bool band) {
+    if (band) return mode == SALOBA_EXTEND ? g1_ptr<1, true>(fmt, false) : g1_ptr<0, true>(fmt, false);
+    return mode == SALOBA_EXTEND ? g1_ptr<1, false>(fmt, qn) : g1_ptr<0, false>(fmt, qn);
 }
 int g1_threads() { return G1_T; }
 int64_t g1_scratch_words(int64_t qcap) { return int64_t(G1_T) * g1_words_per_block() * qcap; }
 
 void launch_dp_g1(int mode, int grid, const AlignArgs& a, int bin, bool qn, cudaStream_t s) {
-    const void* fn = dp_g1_kernel_ptr(mode, a.fmt, qn);
+    const void* fn = dp_g1_kernel_ptr(mode, a.fmt, qn, a.band_w != nullptr);
     AlignArgs args = a;
     void* params[] = {&args, &bin};
     cudaLaunchKernel(fn, dim3(grid), dim3(G1_T), params, 0, s);

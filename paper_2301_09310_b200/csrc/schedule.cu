@@ -128,11 +128,21 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
                 qn = !a.band_w && qn_g <= 1;
                 if (!qn) elig = 0;
             }
+            // NEXT-2 banded pairs: the int16x2 G = 1 kernel (BAND variant) when the band's spill rows
+            // fit its 80-block rows ((2w + 16)/8 + 4 blocks, indexed per strip) and the batch fills the
+            // GPU at one lane per pair (min_gidx == 0: G = 1 on a small batch of long reads left 80% of
+            // the warps idle, measured 0.5 TCUPS in-band on 20k config-4 pairs; Options.force_path = 2
+            // overrides that), else int32 banded
+            if (elig == 1 && a.band_w &&
+                (a.i16_rows == 8 || (a.min_gidx > 0 && a.force_path != 2) ||
+                 min(Q + 1, (2 * min(a.band_w[k], 1 << 20) + 16) / 8 + 4) > qmax_for_gidx(0)))
+                elig = 0;
             const int path = elig ? PATH_I16 : PATH_I32;
-            int g = path == PATH_I16 ? choose_gidx(Q, m, a.force_gidx, a.min_gidx, a.i16_rows, true)
+            int g = (path == PATH_I16 && a.band_w) ? 0
+                    : path == PATH_I16 ? choose_gidx(Q, m, a.force_gidx, a.min_gidx, a.i16_rows, true)
                     : a.band_w        ? choose_gidx_banded(Q, m, a.band_w[k], a.force_gidx)
                                       : choose_gidx(Q, m, a.force_gidx, max(1, a.min_gidx), I32_ROWS, false);  // int32 G=1 measured 3x slower than G=2
-            if (path == PATH_I16 && a.force_gidx < 0 && g >= NGROUPS - 2) {
+            if (path == PATH_I16 && !a.band_w && a.force_gidx < 0 && g >= NGROUPS - 2) {
                 g = NGROUPS - 1;  // the long bin: G=16 or G=32 decided once it is counted
                 atomicMax(a.long_qmax, Q);
             }

@@ -84,10 +84,12 @@ def test_banded_random_schemes_and_bands(sb, mode):
 
 @pytest.mark.parametrize("G", [1, 2, 4, 8, 16, 32])
 def test_banded_across_group_size(sb, G):
+    """The exact int32 banded kernel at every G (force_path=1; int16x2-eligible banded pairs otherwise
+    take the int16x2 G = 1 BAND kernel, tested in test_gpu_banded_i16.py)."""
     b = synth.random_pairs(800, 1, 600, seed=79, p_mut=0.08)
     w = np.random.default_rng(G).integers(0, 120, b.n).astype(np.int32)
     for mode in MODES:
-        got = gpu_banded(sb, b, w, sb.BWA_MEM, mode, sb.Options(force_group=G))
+        got = gpu_banded(sb, b, w, sb.BWA_MEM, mode, sb.Options(force_group=G, force_path=1))
         assert_same(got, oracle_banded(b, w, sb.BWA_MEM, mode), b, w, f"G={G} mode={mode}")
 
 
@@ -145,6 +147,6 @@ def test_banded_extend_large_h0_band_left_edge(sb):
     b.h0[:] = rng.integers(40, 120, b.n).astype(np.int32)
     w = rng.choice(np.array([0, 1, 8, 9, 16, 24], np.int32), b.n)
     for G in (None, 2, 8):
-        opt = sb.Options(force_group=G) if G else None
+        opt = sb.Options(force_group=G, force_path=1) if G else None
         got = gpu_banded(sb, b, w, sb.BWA_MEM, sb.EXTEND, opt)
         assert_same(got, oracle_banded(b, w, sb.BWA_MEM, oracle.EXTEND), b, w, f"left edge G={G}")

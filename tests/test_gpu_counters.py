@@ -74,23 +74,36 @@ def test_step_law(sb, G):
 
 
 def test_lazy_spill_is_one_over_G(sb):
-    """One 2048 x 2048 duo (two identical pairs): 128 strips of 16 rows, Q = 256 blocks."""
+    """SPEC acceptance 4 on a 2048 x 2048 duo (two identical pairs) at G = 32: 128 strips of 16 rows,
+    Q = 256 blocks, 4 chunks; chunk-bottom rows produced = 1/32 of the strips (the rows an eager,
+    every-strip spill would produce), rows spilled = 3 boundaries x Q blocks, steps = 4 x (Q + 31)."""
     rng = np.random.default_rng(2048)
     q = "".join(rng.choice(list("ACGT"), 2048))
     b = synth.from_pairs([(q, q), (q, q)])
-    base = run_counted(sb, b, 1)
-    lazy = run_counted(sb, b, 32)
+    c = run_counted(sb, b, 32)
     Q, strips = 256, 128
-    assert base[0] == strips and lazy[0] == strips // 32
-    # rows produced: 1/G exactly; rows spilled: chunks - 1 boundaries of Q blocks each
-    assert lazy[0] * Q * 32 == base[0] * Q
-    assert base[2] == (strips - 1) * Q and lazy[2] == (strips // 32 - 1) * Q
-    assert lazy[1] == (strips // 32) * (Q + 31)  # the paper's Q + 31
+    assert c[6] == strips and c[0] * 32 == c[6]
+    assert c[2] == (strips // 32 - 1) * Q
+    assert c[1] == (strips // 32) * (Q + 31)
 
 
-@pytest.mark.parametrize("N", [64, 256, 1024])
+def test_spill_g1_vs_g32(sb):
+    """The same 640 x 1024 duo at G = 1 (every strip spills: 63 boundaries) and G = 32 (2 chunks: 1
+    boundary): spilled blocks 63 x 80 vs 1 x 80; rows produced 64 vs 2 = 1/32 (G = 1 takes queries
+    up to 640 bp: its spill rows are sized for 80 blocks)."""
+    rng = np.random.default_rng(640)
+    q = "".join(rng.choice(list("ACGT"), 640))
+    t = "".join(rng.choice(list("ACGT"), 384)) + q
+    b = synth.from_pairs([(q, t), (q, t)])
+    base, lazy = run_counted(sb, b, 1), run_counted(sb, b, 32)
+    assert base[0] == 64 and lazy[0] == 2 and lazy[0] * 32 == base[0]
+    assert base[2] == 63 * 80 and lazy[2] == 1 * 80
+
+
+@pytest.mark.parametrize("N", [64, 256, 640])
 def test_stored_volume_table2(sb, N):
-    """G = 1: spilled bytes per pair = (N/16 - 1) x N x 4 = N^2/4 - 4N (Table II's N^2/4 term)."""
+    """G = 1 (queries up to 640 bp): spilled bytes per pair = (N/16 - 1) x N x 4 = N^2/4 - 4N (Table
+    II's N^2/4 term)."""
     rng = np.random.default_rng(N)
     q = "".join(rng.choice(list("ACGT"), N))
     t = "".join(rng.choice(list("ACGT"), N))

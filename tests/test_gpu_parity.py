@@ -421,3 +421,29 @@ def test_pack_capacity_overflow_reported(sb):
         assert rc == 0 and int(st.item()) == expect
         if expect != -1:
             assert bool((words == 0x7777).all())
+
+
+def test_host_stream_pipelined_batches(sb):
+    """saloba_stream_*: three different batches in flight two at a time give the same results as
+    the device path; an invalid base in the third batch is reported through its own status."""
+    import ctypes
+
+    import torch
+
+    batches = [synth.generate(1, 700, seed=s) for s in (31, 32, 33)]
+    bad = synth.from_pairs([batches[2].pair(k) for k in range(batches[2].n)], batches[2].h0)
+    bad.q_ascii[bad.q_off[412] + 3] = ord("X")
+    batches[2] = bad
+    cap_q = max(len(b.q_ascii) for b in batches) + 64
+    cap_t = max(len(b.t_ascii) for b in batches) + 64
+    hs = sb.HostStream(800, cap_q, cap_t, 300)
+    outs = [torch.empty((3, b.n), dtype=torch.int32, pin_memory=True).numpy() for b in batches]
+    sts = [ctypes.c_int64(99) for _ in batches]
+    for b, o, st in zip(batches, outs, sts):
+        hs.submit(b, o, st, sb.BWA_MEM, sb.EXTEND)
+    hs.wait()
+    assert [st.value for st in sts] == [-1, -1, 412]
+    for b, o in zip(batches[:2], outs[:2]):
+        dev = gpu_align(sb, b, sb.BWA_MEM, 1)
+        assert all(np.array_equal(o[i], dev[i]) for i in range(3))
+    hs.close()
