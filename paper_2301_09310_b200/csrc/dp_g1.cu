@@ -96,6 +96,13 @@ struct G1Band {
     uint32_t wpk, nwpk;           // pack2(wA, wB), pack2(-wA, -wB)
 };
 
+// BAND: in-band flags of an 8 x 16 block whose top-left cell has i - j = d: bit (r - x + 7) is set
+// when |d + r - x| <= w (r - x in [-7, 15]; the block's column x reads bits x .. x + 15 after >> (7 - x))
+__device__ __forceinline__ uint32_t band_bits(int d, int w) {
+    const int lo = max(-w - d, -7) + 7, hi = min(w - d, 15) + 7;
+    return lo > hi ? 0u : ((2u << hi) - 1u) & ~((1u << lo) - 1u);
+}
+
 // One 16-row strip of both halves.
 //   PASS2 = false: returns the lane's maximum of the diagonal candidates D over the strip (max H =
 //     max(0, max D): a positive H reached through a gap is strictly below an earlier cell).
@@ -137,8 +144,9 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
     uint32_t Hl[G1_R], En[G1_R];
 #pragma unroll
     for (int r = 0; r < G1_R; ++r) {
-        const int ha = MODE ? max(0, A.h0 - al - be * (rA + r)) : 0;
-        const int hb = MODE ? max(0, B.h0 - al - be * (rB + r)) : 0;
+        // BAND: H(i, -1) of rows i > w feeds only out-of-band cells; 0 keeps E <= 0 left of the band
+        const int ha = MODE && !(BAND && rA + r > int(bd.wpk & 0xFFFFu)) ? max(0, A.h0 - al - be * (rA + r)) : 0;
+        const int hb = MODE && !(BAND && rB + r > int(bd.wpk >> 16)) ? max(0, B.h0 - al - be * (rB + r)) : 0;
         Hl[r] = pack2(ha, hb);
         En[r] = vadd(Hl[r], nalpha);
     }
@@ -191,9 +199,12 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int j = 8 * s2 + 2 * q;
-                const uint32_t h0v = pack2(MODE ? max(0, A.h0 - al - be * j) : 0, MODE ? max(0, B.h0 - al - be * j) : 0);
-                const uint32_t h1v = pack2(MODE ? max(0, A.h0 - al - be * (j + 1)) : 0,
-                                           MODE ? max(0, B.h0 - al - be * (j + 1)) : 0);
+                // BAND: H(-1, j) of columns j > w feeds only out-of-band cells; 0 keeps F <= 0 above the band
+                const int wA = BAND ? int(bd.wpk & 0xFFFFu) : INT_MAX, wB = BAND ? int(bd.wpk >> 16) : INT_MAX;
+                const uint32_t h0v = pack2(MODE && j <= wA ? max(0, A.h0 - al - be * j) : 0,
+                                           MODE && j <= wB ? max(0, B.h0 - al - be * j) : 0);
+                const uint32_t h1v = pack2(MODE && j + 1 <= wA ? max(0, A.h0 - al - be * (j + 1)) : 0,
+                                           MODE && j + 1 <= wB ? max(0, B.h0 - al - be * (j + 1)) : 0);
                 st.top[slot][q][tid] = make_uint4(h0v, noGap, h1v, noGap);
             }
         }
@@ -201,8 +212,9 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int j = 8 * s2 + 2 * q;
-                st.top[2 + slot][q][tid] = make_uint4(pack2(0, MODE ? max(0, B.h0 - al - be * j) : 0), noGap,
-                                                      pack2(0, MODE ? max(0, B.h0 - al - be * (j + 1)) : 0), noGap);
+                const int wB = BAND ? int(bd.wpk >> 16) : INT_MAX;
+                st.top[2 + slot][q][tid] = make_uint4(pack2(0, MODE && j <= wB ? max(0, B.h0 - al - be * j) : 0), noGap,
+                                                      pack2(0, MODE && j + 1 <= wB ? max(0, B.h0 - al - be * (j + 1)) : 0), noGap);
             }
         }
         if (BAND) {  // top-row blocks the strip above never computed are out of band: H = F = 0
@@ -321,7 +333,7 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                 uint32_t haup = vadd(hup, nalpha);
                 uint32_t hdiag = hdiag_top;
                 hdiag_top = hup;
-                uint32_t nm = 0;
+                [[maybe_unused]] uint32_t nm = 0;
                 if constexpr (QN) nm = prmt(sel[x], 0u, 0x3322);  // 0xFFFF per half whose column is N
                 uint32_t dprev = 0;
     #pragma unroll
@@ -376,82 +388,96 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
             }
             corner = hdiag_top;
         };
-        // Band-edge steps take a compact variant (columns in a rolled loop): a second fully unrolled
-        // body made the step code too large for the instruction cache (ncu: 44% no-instruction stalls)
+        // Band-edge steps take a compact variant (column pairs in a rolled loop: a second fully
+        // unrolled body made the step code too large for the instruction cache, ncu: 44% no-instruction
+        // stalls).  Only H is masked to 0 out of band: E and F there may hold garbage, which never
+        // reaches the band (E moves right, F down: out of band right of / below the band they only
+        // leave it; left of / above it H = 0 and the boundary inputs are <= 0, so E, F <= 0 there,
+        // and a non-positive E or F never changes any H = max(0, ...) — S:142-143).  The lane maximum
+        // tracks the masked H instead of D (same value: max H = max(0, max D)).
         auto edge_body = [&]() {
+            const uint32_t wbA = band_bits(rA - 8 * s, int(bd.wpk & 0xFFFFu));
+            const uint32_t wbB = band_bits(rB - 8 * s, int(bd.wpk >> 16));
             uint32_t hdiag_top = corner;
 #pragma unroll 1
-            for (int x = 0; x < 8; ++x) {
-                const uint4 tqx = st.top[slot][x >> 1][tid];
-                uint32_t hup = (x & 1) ? tqx.z : tqx.x, fup = (x & 1) ? tqx.w : tqx.y;
-                if (PASS2 && split) {
-                    const uint4 tbx = st.top[2 + slot][x >> 1][tid];
-                    hup = prmt(hup, (x & 1) ? tbx.z : tbx.x, 0x7610);
-                    fup = prmt(fup, (x & 1) ? tbx.w : tbx.y, 0x7610);
+            for (int p = 0; p < 4; ++p) {
+                const uint4 tqp = st.top[slot][p][tid];
+                uint4 tbp = tqp;
+                if (PASS2 && split) tbp = st.top[2 + slot][p][tid];
+                uint32_t se = sel[0], so = sel[1];
+#pragma unroll
+                for (int k = 1; k < 4; ++k) {
+                    se = p == k ? sel[2 * k] : se;
+                    so = p == k ? sel[2 * k + 1] : so;
                 }
-                uint32_t selx = sel[0];
+                uint32_t bh[2], bf[2];
 #pragma unroll
-                for (int k = 1; k < 8; ++k) selx = x == k ? sel[k] : selx;
-                uint32_t haup = vadd(hup, nalpha);
-                uint32_t hdiag = hdiag_top;
-                hdiag_top = hup;
-                const uint32_t tx = vadd(dpk, pack2(-x, -x));
-                uint32_t dprev = 0;
+                for (int xx = 0; xx < 2; ++xx) {
+                    const int x = 2 * p + xx;
+                    uint32_t hup = xx ? tqp.z : tqp.x, fup = xx ? tqp.w : tqp.y;
+                    if (PASS2 && split) {
+                        hup = prmt(hup, xx ? tbp.z : tbp.x, 0x7610);
+                        fup = prmt(fup, xx ? tbp.w : tbp.y, 0x7610);
+                    }
+                    const uint32_t selx = xx ? so : se;
+                    // in-band rows of column x: bit r (half A) / bit 16 + r (half B)
+                    const uint32_t m = prmt(wbA >> (7 - x), wbB >> (7 - x), 0x5410);
+                    uint32_t haup = vadd(hup, nalpha);
+                    uint32_t hdiag = hdiag_top;
+                    hdiag_top = hup;
+                    uint32_t hprev = 0;
 #pragma unroll
-                for (int r = 0; r < G1_R; ++r) {
-                    const uint32_t f = vaddmax(fup, nbeta, haup);
-                    const uint32_t e = En[r];
-                    const uint32_t scv = prmt(tabA[r], tabB[r], selx);
-                    uint32_t d = MODE ? vaddmin(hdiag, scv, hdiag * lam) : vadd(hdiag, scv);
-                    uint32_t h = vmax3relu(d, e, f);
-                    const uint32_t t = vadd(tx, pack2(r, r));
-                    const uint32_t mk = __vcmples2(t, bd.wpk) & __vcmpges2(t, bd.nwpk);
-                    h &= mk;
-                    d &= mk;
-                    hdiag = Hl[r];
-                    Hl[r] = h;
-                    En[r] = vaddmax(e & mk, nbeta, vadd(h, nalpha));
-                    hup = h;
-                    haup = vadd(h, nalpha);
-                    fup = f & mk;
-                    if (!PASS2) {
-                        if (r & 1) {
-                            if ((r & 7) == 1) M0 = vmax3(M0, dprev, d);
-                            if ((r & 7) == 3) M1 = vmax3(M1, dprev, d);
-                            if ((r & 7) == 5) M2 = vmax3(M2, dprev, d);
-                            if ((r & 7) == 7) M3 = vmax3(M3, dprev, d);
+                    for (int r = 0; r < G1_R; ++r) {
+                        const uint32_t f = vaddmax(fup, nbeta, haup);
+                        const uint32_t e = En[r];
+                        const uint32_t scv = prmt(tabA[r], tabB[r], selx);
+                        const uint32_t d = MODE ? vaddmin(hdiag, scv, hdiag * lam) : vadd(hdiag, scv);
+                        // bits r and 16 + r moved to the sign bits of the halves, replicated by PRMT
+                        const uint32_t h = vmax3relu(d, e, f) & prmt(m << (15 - r), 0u, 0xbb99);
+                        hdiag = Hl[r];
+                        Hl[r] = h;
+                        En[r] = vaddmax(e, nbeta, vadd(h, nalpha));
+                        hup = h;
+                        haup = vadd(h, nalpha);
+                        fup = f;
+                        if (!PASS2) {
+                            if (r & 1) {
+                                if ((r & 7) == 1) M0 = vmax3(M0, hprev, h);
+                                if ((r & 7) == 3) M1 = vmax3(M1, hprev, h);
+                                if ((r & 7) == 5) M2 = vmax3(M2, hprev, h);
+                                if ((r & 7) == 7) M3 = vmax3(M3, hprev, h);
+                            }
+                            hprev = h;
                         }
-                        dprev = d;
                     }
-                }
+                    bh[xx] = hup;
+                    bf[xx] = fup;
+                    if (PASS2) {
+                        uint32_t cm = vmax3(vmax3(Hl[0], Hl[1], Hl[2]), vmax3(Hl[3], Hl[4], Hl[5]), vmax3(Hl[6], Hl[7], Hl[8]));
+                        cm = vmax3(cm, vmax3(Hl[9], Hl[10], Hl[11]), vmax3(Hl[12], Hl[13], Hl[14]));
+                        cm = vmax(cm, Hl[15]);
+                        if (lo16(cm) >= lo16(target) || hi16(cm) >= hi16(target)) {
+                            uint32_t bits = 0;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    if (x == k) {
-                        botH[k] = hup;
-                        botF[k] = fup;
+                            for (int r = 0; r < G1_R; ++r) bits |= eq_bits(Hl[r], target, r);
+                            take_hit(bits, 8 * s + x, rA, rB, hit);
+                        }
                     }
                 }
-                if (PASS2) {
-                    uint32_t cm = vmax3(vmax3(Hl[0], Hl[1], Hl[2]), vmax3(Hl[3], Hl[4], Hl[5]), vmax3(Hl[6], Hl[7], Hl[8]));
-                    cm = vmax3(cm, vmax3(Hl[9], Hl[10], Hl[11]), vmax3(Hl[12], Hl[13], Hl[14]));
-                    cm = vmax(cm, Hl[15]);
-                    if (lo16(cm) >= lo16(target) || hi16(cm) >= hi16(target)) {
-                        uint32_t bits = 0;
-#pragma unroll
-                        for (int r = 0; r < G1_R; ++r) bits |= eq_bits(Hl[r], target, r);
-                        take_hit(bits, 8 * s + x, rA, rB, hit);
-                    }
-                }
+                if (bot >= 0) *sc.row_at(bot, s - bd.wbase, p) = make_uint4(bh[0], bf[0], bh[1], bf[1]);
             }
             corner = hdiag_top;
         };
-        if (BAND && edge) edge_body();
-        else step_body(std::false_type{});
-        if (bot >= 0) {
+        if (BAND && edge) {
+            edge_body();
+        } else {
+            step_body(std::false_type{});
+            if (bot >= 0) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                *sc.row_at(bot, BAND ? s - bd.wbase : s, q) =
-                    make_uint4(botH[2 * q], botF[2 * q], botH[2 * q + 1], botF[2 * q + 1]);
+                for (int q = 0; q < 4; ++q)
+                    *sc.row_at(bot, BAND ? s - bd.wbase : s, q) =
+                        make_uint4(botH[2 * q], botF[2 * q], botH[2 * q + 1], botF[2 * q + 1]);
+            }
         }
     }
     return vmax(vmax(M0, M1), vmax(M2, M3));
