@@ -440,7 +440,7 @@ def main():
             hs.wait()
 
         e2e_val = timed(stream_steps)
-        assert sts[0].value == -1 and sts[1].value == -1
+        assert all(sts[k].value == -1 for k in range(min(2, args.e2e_steps))), [x.value for x in sts]
         hs.close()
         # (b) one synchronous call per batch (saloba_align_host_ctx, 4 pipelined slices inside a batch)
         out = outs[0]
