@@ -583,9 +583,10 @@ def main():
             "frac": round(achieved / peak, 4), "traffic": traffic,
             "kernel": ("dp_i16_kernel" if path == "int16x2" else "dp_i32_kernel") +
                       " (all bins of one call, CUDA events on the launching stream)",
-            # bin 13 = the int16x2 long bin, run at G = 2^long_group (16 or 32) this call
+            # bin 13 = the int16x2 long bin, run at G = 2^long_group (16 or 32) this call, or (6) on the
+            # cooperative kernel (several warps per duo)
             "bins": {("i16_G1_queryN" if b == 14 else "i16_G2_queryN" if b == 6 else
-                      f"{'i16' if b >= 8 else 'i32'}_G{1 << (lg if b == 13 else b % 8)}{'_long' if b == 13 else ''}"): c
+                      (f"{'i16' if b >= 8 else 'i32'}_G{1 << (lg if b == 13 else b % 8)}{'_long' if b == 13 else ''}" if not (b == 13 and lg == 6) else "i16_long_coop")): c
                      for b, c in enumerate(bc) if c and b != 15},
             "dp_share_of_step": round(dp_ms_avg / ms_per_step, 3),
             "peak_derivation": f"{sms} SMs x {f_mhz:.0f} MHz (median under load) x {p_int:.0f} int lane-ops/clk/SM "

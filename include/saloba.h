@@ -102,9 +102,11 @@ typedef struct {
                              Bins 14 / 6: int16x2 G=1 / G=2 pairs whose query contains N (an N
                              column's substitution is forced to mismatch; other query-N pairs run
                              int32).  Bin 7: int32 pairs whose values could reach 2^27 */
-    int32_t* long_group;  /* optional [dev] int32[1]: log2(G) the long bin ran with this call (4 or 5):
-                             G=16 iff the bin holds >= 4 waves of G=16 subwarps (throughput), else
-                             G=32 (half the per-pair latency: few long pairs finish sooner) */
+    int32_t* long_group;  /* optional [dev] int32[1]: how the long bin ran this call: 4 or 5 = log2(G)
+                             of the one-warp-per-duo kernel (G=16 iff the bin holds >= 4 waves of
+                             G=16 subwarps, else G=32: half the per-pair latency), 6 = the cooperative
+                             kernel (fewer long pairs than two waves of G=32 warps hold: the warps of a
+                             block share each duo, one 512-row chunk each) */
     unsigned long long* counters; /* optional [dev] uint64[8], ADDED to (SURVEY §8(f) NEXT-4 instrumentation
                              of the int16x2 kernels, §IV-A / SPEC acceptance 3-5): [0] pass-1
                              chunk passes of all work items (a work item = two pairs, one per 16-bit

@@ -17,7 +17,7 @@ static std::atomic<long long> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 cudaError_t run_classify_sort(const ClassifyArgs& ca, const SortKV& kv, int32_t* bin_start, int sms,
-                              int32_t* long_gidx, int64_t cap16, cudaStream_t s);
+                              int32_t* long_gidx, int64_t cap16, int64_t coop_pairs, cudaStream_t s);
 size_t cub_sort_temp_bytes(int64_t n);
 void launch_status_init(int64_t* st, cudaStream_t s);
 void launch_status_final(int64_t* st, cudaStream_t s);
@@ -29,6 +29,10 @@ const void* dp_i16_qn_kernel_ptr(int mode, int rows, int gidx);
 void launch_dp_i16_qn(int mode, int gidx, int grid, const AlignArgs& a, cudaStream_t s);
 const void* dp_g1_kernel_ptr(int mode, int fmt, bool qn, bool band);
 int g1_threads();
+const void* dp_coop_kernel_ptr(int mode, int fmt);
+void launch_dp_coop(int mode, int grid, const AlignArgs& a, cudaStream_t s);
+size_t g1_smem_bytes(bool qn);
+void g1_set_smem_attrs();
 int64_t g1_scratch_words(int64_t qcap);
 void launch_dp_g1(int mode, int grid, const AlignArgs& a, int bin, bool qn, cudaStream_t s);
 // the G = 1 int16x2 bins run the dedicated kernel of dp_g1.cu (16-row strips, banded variant);
@@ -52,6 +56,7 @@ struct DevInfo {
     int blocks_i16[2][2][NGROUPS] = {};  // [rows 8|16][mode][gidx]
     int blocks_i16qn[2][2][2] = {};      // QN variant: [rows 8|16][mode][G = 1|2]
     int blocks_g1[2][2] = {};            // dp_g1 kernel: [mode][QN]
+    int blocks_coop[2] = {};             // dp_coop_kernel (cooperative long pairs): [mode]
     int max_blocks_per_sm = 1;           // max resident blocks of any DP kernel (block-slot pool)
 };
 constexpr int NAUX = 4;
@@ -91,14 +96,21 @@ static const DevInfo* dev_info(int device) {
                     }
                 }
             }
+        g1_set_smem_attrs();
+        for (int mode = 0; mode < 2; ++mode) {
+            int nb = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_coop_kernel_ptr(mode, SALOBA_PACK4), I16_THREADS, 0);
+            d.blocks_coop[mode] = std::max(1, nb);
+            d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_coop[mode]);
+        }
         for (int mode = 0; mode < 2; ++mode)
             for (int qn = 0; qn < 2; ++qn) {
                 int nb = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_g1_kernel_ptr(mode, SALOBA_PACK4, qn != 0, false),
-                                                              g1_threads(), 0);
+                                                              g1_threads(), g1_smem_bytes(qn != 0));
                 int nbb = 0;  // the banded variant (NEXT-2): the grid takes the smaller occupancy
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, dp_g1_kernel_ptr(mode, SALOBA_PACK4, false, true),
-                                                              g1_threads(), 0);
+                                                              g1_threads(), g1_smem_bytes(false));
                 if (nbb > 0) nb = std::min(nb, nbb);
                 d.blocks_g1[mode][qn] = std::max(1, nb);
                 d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_g1[mode][qn]);
@@ -331,7 +343,11 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
                     o.force_path, o.keep_order, i16_rows, Qsup * 8, score, q_end, t_end, kv.keys_in,
                     kv.vals_in, bin_count, (unsigned long long*)status, long_qmax, band_w, i32_fast, min_gidx};
     const int64_t cap16 = int64_t(grid_for(d, int(mode), PATH_I16, NGROUPS - 2, i16_rows)) * (I16_THREADS / 16) * 2;
-    if (run_classify_sort(ca, kv, bin_start, d->sms, long_gidx, cap16, s) != cudaSuccess) return SALOBA_ECUDA;
+    // cooperative long-pair kernel below two waves of one-warp duos (SALOBA_COOP_PAIRS overrides: 0 = off)
+    int64_t coop_pairs = int64_t(d->sms) * d->blocks_i16[1][int(mode)][NGROUPS - 1] * (I16_THREADS / 32) * 2 * 2;
+    if (const char* e = getenv("SALOBA_COOP_PAIRS")) coop_pairs = atoll(e);
+    if (i16_rows != 16) coop_pairs = 0;  // the cooperative kernel is built for 16-row strips
+    if (run_classify_sort(ca, kv, bin_start, d->sms, long_gidx, cap16, coop_pairs, s) != cudaSuccess) return SALOBA_ECUDA;
 
     if (n_pairs > 0) {
         AlignArgs a{};
@@ -373,6 +389,8 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
                     AlignArgs a16 = a;
                     a16.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(g - 1), Qsup) + 8;
                     launch_dp_i16(int(mode), g - 1, grid_for(d, int(mode), path, g - 1, i16_rows), a16, LONG_BIN, as);
+                    // ... and the cooperative kernel (the long bin's spill stride of G = 32)
+                    if (i16_rows == 16) launch_dp_coop(int(mode), d->sms * d->blocks_coop[int(mode)], a, as);
                 } else if (path == PATH_I16 && g == 0 && use_g1(i16_rows)) {
                     AlignArgs a1 = a;
                     a1.spill_stride = std::min<int64_t>(qmax_for_gidx(0), Qsup);  // dp_g1: query-block capacity

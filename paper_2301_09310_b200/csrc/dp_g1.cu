@@ -24,6 +24,7 @@
 // Cell update per 32-bit register (2 cells, one per pair of the duo): see dp_i16.cu.
 // Exactness of the 16-bit lanes is guaranteed by routing (schedule.cu): scores fit int8 and all
 // H, E, F stay inside int16 (SURVEY §8(c) reading 8).
+#include <cstddef>
 #include <type_traits>
 
 #include "dp_i16_common.cuh"
@@ -32,7 +33,10 @@ namespace saloba {
 
 constexpr int G1_T = 128;    // threads per block
 constexpr int G1_R = 16;     // target rows per strip (two packed target words per half)
-constexpr int G1_DEPTH = 3;  // stage slots in pass 1 (inputs requested two steps ahead)
+#ifndef G1_DEPTH_CFG
+#define G1_DEPTH_CFG 4
+#endif
+constexpr int G1_DEPTH = G1_DEPTH_CFG;  // stage slots in pass 1 (inputs requested DEPTH-1 steps ahead)
 constexpr int G1_NBUF = 4;   // spill buffers per thread: read, write, two checkpoints
 // Resident blocks per SM: 3.  Not register-bound: the spill rows of all resident threads must stay
 // L2-resident between a chunk writing them and the next chunk reading them (reuse distance =
@@ -44,12 +48,30 @@ constexpr int G1_MINB = 3;
 // no N) + G1_NBUF spill rows of 16 words.
 __host__ __device__ constexpr int g1_words_per_block() { return 8 + G1_NBUF * 16; }
 
+// pass-1 stage depth: the QN variant keeps 3 (its 8-word selectors double the selector rows)
+template <bool QN>
+__host__ __device__ constexpr int g1_depth() { return QN && G1_DEPTH > 3 ? 3 : G1_DEPTH; }
+#ifndef G1_ROLL
+#define G1_ROLL 1
+#endif
+#ifndef G1_DEPTH2_CFG
+#define G1_DEPTH2_CFG 2
+#endif
+// Per-block stage in dynamic shared memory: ENTRY rows of one uint4 per thread ([entry][G1_T]), so
+// thread t owns column t in every layout and pass 1 and pass 2 (a block's threads may be in either)
+// can number the rows differently over the same bytes.  Per pass, with D stage slots:
+//   sel(slot, h) = slot*NS + h        the step's selectors (QN: 8 words with N flags, NS = 2;
+//                                     otherwise 8 compact 16-bit selectors, NS = 1)
+//   q(slot)      = D*NS + slot        chunk 0 / banded: the step's packed query words (.x A, .y B)
+//   top(slot, q) = D*(NS+1) + 4*slot + q   top-row quads (H[2q], F[2q], H[2q+1], F[2q+1]); pass 2
+//                                     stages half B's checkpoint row in slots D..2D-1
+template <bool QN>
 struct G1Stage {
-    uint4 sel[G1_DEPTH][2][G1_T];   // chunks >= 1 and pass 2: the step's selectors (QN: 8 words
-                                    // with N flags; otherwise [0] holds 8 compact 16-bit selectors)
-    uint32_t q[G1_DEPTH][2][G1_T];  // chunk 0: the step's packed query words (halves A, B)
-    uint4 top[4][4][G1_T];          // top-row quads (H[2q], F[2q], H[2q+1], F[2q+1]);
-                                    // pass 1: slots 0..2; pass 2: A slots 0..1, B slots 2..3
+    static constexpr int D = g1_depth<QN>();  // pass 1
+    static constexpr int D2 = G1_DEPTH2_CFG;   // pass 2
+    static constexpr int NS = QN ? 2 : 1;
+    static constexpr int E1 = D * (NS + 1) + 4 * D, E2 = D2 * (NS + 1) + 8 * D2;
+    uint4 e[E1 > E2 ? E1 : E2][G1_T];
 };
 
 // Scratch of one thread slot inside the block's pool slot:
@@ -110,17 +132,19 @@ __device__ __forceinline__ uint32_t band_bits(int d, int w) {
 //   selgen: build the selectors from the query words and store them (chunk 0 of pass 1).
 //   topA / topB: spill buffer of the top row per half (-1: the table boundary); bot: buffer that
 //     receives the bottom row (-1: none).
+//   HOT: pass 1 below chunk 0 without a band (the bulk of the work): compile-time selgen = false and
+//     top row from the spill buffer, so the step loop carries no boundary or selector-build code.
 //   BAND: only cells |i - j| <= w (per half) are in the table; the strip runs steps
 //     [bd.s_begin, bd.s_end] (a corner visit + the union of the warp's band blocks), blocks that
 //     cross a band edge mask their out-of-band cells to H = E = F = 0, selectors are built every
 //     step (no selector scratch), and spill rows are indexed relative to the writing strip's first
 //     step so a row needs ~(2w + 16)/8 + 3 blocks whatever the query length.
-template <int MODE, int FMT, bool PASS2, bool QN, bool BAND = false>
+template <int MODE, int FMT, bool PASS2, bool QN, bool BAND = false, bool HOT = false>
 __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, const HalfInfo& A, const HalfInfo& B,
                                              const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
                                              const int rA, const int rB, const int topA, const int topB,
-                                             const int bot, const bool selgen, const uint32_t target,
-                                             int (&hit)[4], G1Stage& st, const G1Scratch& sc,
+                                             const int bot, const bool selgen_rt, const uint32_t target,
+                                             int (&hit)[4], G1Stage<QN>& st, const G1Scratch& sc,
                                              const uint32_t (&twraw)[4], const G1Band& bd) {
     const int tid = threadIdx.x;
     const int al = a.alpha, be = a.beta;
@@ -157,30 +181,47 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
         corner = pack2(ca, cb);
     }
     uint32_t M0 = 0, M1 = 0, M2 = 0, M3 = 0;
-    constexpr int DEPTH = PASS2 ? 2 : G1_DEPTH;
-    const bool topA_mem = topA >= 0;
+    constexpr int DEPTH = PASS2 ? G1Stage<QN>::D2 : G1Stage<QN>::D;
+    constexpr int NS = G1Stage<QN>::NS;
+    constexpr int BOFF = DEPTH;  // pass 2: stage slot of half B's top row = BOFF + slot
+    constexpr int Q0 = DEPTH * NS, T0 = DEPTH * (NS + 1);  // first q / top entry rows
+    auto ENT = [&](int e) -> uint4& { return st.e[e][tid]; };
+    auto TOP = [&](int slot, int q) -> uint4& { return ENT(T0 + slot * 4 + q); };
+    static_assert(!HOT || (!PASS2 && !BAND), "HOT is the unbanded pass-1 strip");
+    const bool selgen = HOT ? false : selgen_rt;
+    const bool topA_mem = HOT ? true : topA >= 0;
     const bool topB_mem = PASS2 && topB >= 0 && topB != topA;
     const bool split = PASS2 && (topB != topA || rB != rA);  // pass 2 halves at different chunks
     const int s_last = BAND ? bd.s_end : Q - 1;
+    // shared-space addresses of this thread's stage entries and the global bases of its rows, once
+    // per strip (the per-step generic-to-shared conversion re-read the CTA id: an S2UR stall per step)
+    const uint32_t st_s = static_cast<uint32_t>(__cvta_generic_to_shared(&st));
+    const uint32_t s_ent = st_s + tid * 16;  // + entry * G1_T*16
+    const uint4* const g_sel = sc.sel_at(0, 0);                                 // + s * 2*G1_T*16 B
+    const uint4* const g_topA = sc.row_at(topA_mem ? topA : 0, 0, 0);           // + idx * 64 B
+    const uint4* const g_topB = sc.row_at(topB_mem ? topB : 0, 0, 0);
+    uint4* const g_bot = sc.row_at(bot >= 0 ? bot : 0, 0, 0);
+    constexpr uint32_t str64 = 64, str_sel = 2 * G1_T * 16;
     auto prefetch = [&](int s2, int slot) {
         if (s2 <= s_last) {
             if (selgen) {
                 const int wi = FMT == SALOBA_PACK2 ? (s2 >> 1) : s2;
-                if (8 * s2 < A.n) cp_async4(&st.q[slot][0][tid], qwA + wi);
-                if (8 * s2 < B.n) cp_async4(&st.q[slot][1][tid], qwB + wi);
+                if (8 * s2 < A.n) cp_async4s(s_ent + (Q0 + slot) * (G1_T * 16), qwA + wi);
+                if (8 * s2 < B.n) cp_async4s(s_ent + (Q0 + slot) * (G1_T * 16) + 4, qwB + wi);
             } else {
-                cp_async16(&st.sel[slot][0][tid], sc.sel_at(s2, 0));
-                if (QN) cp_async16(&st.sel[slot][1][tid], sc.sel_at(s2, 1));
+                const uint4* g = wide_at(g_sel, s2, str_sel);
+                cp_async16s(s_ent + (slot * NS) * (G1_T * 16), g);
+                if (QN) cp_async16s(s_ent + (slot * NS + 1) * (G1_T * 16), g + G1_T);
             }
             if (topA_mem && (!BAND || s2 <= bd.hiA)) {
+                const uint4* g = wide_at(g_topA, BAND ? s2 - bd.rbaseA : s2, str64);
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    cp_async16(&st.top[slot][q][tid], sc.row_at(topA, BAND ? s2 - bd.rbaseA : s2, q));
+                for (int q = 0; q < 4; ++q) cp_async16s(s_ent + (T0 + slot * 4 + q) * (G1_T * 16), g + q);
             }
             if (topB_mem && (!BAND || s2 <= bd.hiB)) {
+                const uint4* g = wide_at(g_topB, BAND ? s2 - bd.rbaseB : s2, str64);
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    cp_async16(&st.top[2 + slot][q][tid], sc.row_at(topB, BAND ? s2 - bd.rbaseB : s2, q));
+                for (int q = 0; q < 4; ++q) cp_async16s(s_ent + (T0 + (BOFF + slot) * 4 + q) * (G1_T * 16), g + q);
             }
         }
         cp_async_commit();
@@ -205,7 +246,7 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                                            MODE && j <= wB ? max(0, B.h0 - al - be * j) : 0);
                 const uint32_t h1v = pack2(MODE && j + 1 <= wA ? max(0, A.h0 - al - be * (j + 1)) : 0,
                                            MODE && j + 1 <= wB ? max(0, B.h0 - al - be * (j + 1)) : 0);
-                st.top[slot][q][tid] = make_uint4(h0v, noGap, h1v, noGap);
+                TOP(slot, q) = make_uint4(h0v, noGap, h1v, noGap);
             }
         }
         if (PASS2 && split && !topB_mem) {
@@ -213,29 +254,30 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
             for (int q = 0; q < 4; ++q) {
                 const int j = 8 * s2 + 2 * q;
                 const int wB = BAND ? int(bd.wpk >> 16) : INT_MAX;
-                st.top[2 + slot][q][tid] = make_uint4(pack2(0, MODE && j <= wB ? max(0, B.h0 - al - be * j) : 0), noGap,
+                TOP(BOFF + slot, q) = make_uint4(pack2(0, MODE && j <= wB ? max(0, B.h0 - al - be * j) : 0), noGap,
                                                       pack2(0, MODE && j + 1 <= wB ? max(0, B.h0 - al - be * (j + 1)) : 0), noGap);
             }
         }
         if (BAND) {  // top-row blocks the strip above never computed are out of band: H = F = 0
             if (topA_mem && s2 > bd.hiA) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) st.top[slot][q][tid] = make_uint4(0, 0, 0, 0);
+                for (int q = 0; q < 4; ++q) TOP(slot, q) = make_uint4(0, 0, 0, 0);
             }
             if (PASS2 && split && topB_mem && s2 > bd.hiB) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) st.top[2 + slot][q][tid] = make_uint4(0, 0, 0, 0);
+                for (int q = 0; q < 4; ++q) TOP(BOFF + slot, q) = make_uint4(0, 0, 0, 0);
             }
         }
         if (selgen) {
-            nq0 = st.q[slot][0][tid];
-            nq1 = st.q[slot][1][tid];
+            const uint4 qq = ENT(Q0 + slot);
+            nq0 = qq.x;
+            nq1 = qq.y;
         } else {
-            nsel0 = st.sel[slot][0][tid];
-            if (QN) nsel1 = st.sel[slot][1][tid];
+            nsel0 = ENT(slot * NS);
+            if constexpr (QN) nsel1 = ENT(slot * NS + 1);
         }
-        ntq = st.top[slot][0][tid];
-        if (PASS2 && split) ntb = st.top[2 + slot][0][tid];
+        ntq = TOP(slot, 0);
+        if (PASS2 && split) ntb = TOP(BOFF + slot, 0);
     };
 
     int cur = 0;
@@ -246,9 +288,9 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
             // corner visit of the block left of the band: nothing computed; the corner of the first
             // band block is this block's top-row H at its last column, and the column left of the
             // band is out of band for every row of the strip (H = E = 0)
-            const uint4 t3 = st.top[cur][3][tid];
+            const uint4 t3 = TOP(cur, 3);
             corner = t3.z;
-            if (PASS2 && split) corner = prmt(corner, st.top[2 + cur][3][tid].z, 0x7610);
+            if (PASS2 && split) corner = prmt(corner, TOP(BOFF + cur, 3).z, 0x7610);
 #pragma unroll
             for (int r = 0; r < G1_R; ++r) {
                 Hl[r] = 0;
@@ -319,8 +361,8 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                         tq = tqn;
                         if (PASS2 && split) tb = tbn;
                         if (x + 2 < 8) {
-                            tqn = st.top[slot][(x >> 1) + 1][tid];
-                            if (PASS2 && split) tbn = st.top[2 + slot][(x >> 1) + 1][tid];
+                            tqn = TOP(slot, (x >> 1) + 1);
+                            if (PASS2 && split) tbn = TOP(BOFF + slot, (x >> 1) + 1);
                         }
                     }
                     hup = (x & 1) ? tq.z : tq.x;
@@ -395,15 +437,20 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
         // leave it; left of / above it H = 0 and the boundary inputs are <= 0, so E, F <= 0 there,
         // and a non-positive E or F never changes any H = max(0, ...) — S:142-143).  The lane maximum
         // tracks the masked H instead of D (same value: max H = max(0, max D)).
-        auto edge_body = [&]() {
-            const uint32_t wbA = band_bits(rA - 8 * s, int(bd.wpk & 0xFFFFu));
-            const uint32_t wbB = band_bits(rB - 8 * s, int(bd.wpk >> 16));
+        // MASK = false: the same compact body without band masking, for the strips outside the hot
+        // pass-1 loop (chunk 0, pass 2; G1_ROLL): their steps are 1/8 of the work, and a second and
+        // third fully unrolled body made the kernel's hot code outgrow the instruction cache (ncu:
+        // no-instruction stalls at every branch of pass 2's unrolled body)
+        auto edge_body = [&](auto mask_tag) {
+            constexpr bool MASK = decltype(mask_tag)::value;
+            const uint32_t wbA = MASK ? band_bits(rA - 8 * s, int(bd.wpk & 0xFFFFu)) : 0u;
+            const uint32_t wbB = MASK ? band_bits(rB - 8 * s, int(bd.wpk >> 16)) : 0u;
             uint32_t hdiag_top = corner;
 #pragma unroll 1
             for (int p = 0; p < 4; ++p) {
-                const uint4 tqp = st.top[slot][p][tid];
+                const uint4 tqp = TOP(slot, p);
                 uint4 tbp = tqp;
-                if (PASS2 && split) tbp = st.top[2 + slot][p][tid];
+                if (PASS2 && split) tbp = TOP(BOFF + slot, p);
                 uint32_t se = sel[0], so = sel[1];
 #pragma unroll
                 for (int k = 1; k < 4; ++k) {
@@ -421,7 +468,9 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                     }
                     const uint32_t selx = xx ? so : se;
                     // in-band rows of column x: bit r (half A) / bit 16 + r (half B)
-                    const uint32_t m = prmt(wbA >> (7 - x), wbB >> (7 - x), 0x5410);
+                    const uint32_t m = MASK ? prmt(wbA >> (7 - x), wbB >> (7 - x), 0x5410) : 0u;
+                    [[maybe_unused]] uint32_t nm = 0;
+                    if constexpr (QN) nm = prmt(selx, 0u, 0x3322);  // 0xFFFF per half whose column is N
                     uint32_t haup = vadd(hup, nalpha);
                     uint32_t hdiag = hdiag_top;
                     hdiag_top = hup;
@@ -430,10 +479,12 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                     for (int r = 0; r < G1_R; ++r) {
                         const uint32_t f = vaddmax(fup, nbeta, haup);
                         const uint32_t e = En[r];
-                        const uint32_t scv = prmt(tabA[r], tabB[r], selx);
+                        uint32_t scv = prmt(tabA[r], tabB[r], selx);
+                        if constexpr (QN) scv = (scv & ~nm) | (mmw & nm);
                         const uint32_t d = MODE ? vaddmin(hdiag, scv, hdiag * lam) : vadd(hdiag, scv);
                         // bits r and 16 + r moved to the sign bits of the halves, replicated by PRMT
-                        const uint32_t h = vmax3relu(d, e, f) & prmt(m << (15 - r), 0u, 0xbb99);
+                        uint32_t h = vmax3relu(d, e, f);
+                        if constexpr (MASK) h &= prmt(m << (15 - r), 0u, 0xbb99);
                         hdiag = Hl[r];
                         Hl[r] = h;
                         En[r] = vaddmax(e, nbeta, vadd(h, nalpha));
@@ -464,19 +515,20 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                         }
                     }
                 }
-                if (bot >= 0) *sc.row_at(bot, s - bd.wbase, p) = make_uint4(bh[0], bf[0], bh[1], bf[1]);
+                if (bot >= 0) st_global16(wide_at(g_bot, s - bd.wbase, str64) + p, make_uint4(bh[0], bf[0], bh[1], bf[1]));
             }
             corner = hdiag_top;
         };
         if (BAND && edge) {
-            edge_body();
+            edge_body(std::true_type{});
+        } else if (!HOT && !BAND && G1_ROLL) {
+            edge_body(std::false_type{});
         } else {
             step_body(std::false_type{});
             if (bot >= 0) {
+                uint4* g = wide_at(g_bot, BAND ? s - bd.wbase : s, str64);
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    *sc.row_at(bot, BAND ? s - bd.wbase : s, q) =
-                        make_uint4(botH[2 * q], botF[2 * q], botH[2 * q + 1], botF[2 * q + 1]);
+                for (int q = 0; q < 4; ++q) st_global16(g + q, make_uint4(botH[2 * q], botF[2 * q], botH[2 * q + 1], botF[2 * q + 1]));
             }
         }
     }
@@ -517,7 +569,8 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
         sc.sel = pool;
         sc.row = pool + size_t(sc.qcap) * 2 * G1_T;
     }
-    __shared__ G1Stage st;
+    extern __shared__ __align__(16) unsigned char g1_smem[];
+    G1Stage<QN>& st = *reinterpret_cast<G1Stage<QN>*>(g1_smem);
 
     for (;;) {
         int base = 0;
@@ -580,9 +633,14 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
                 bd.hiA = bd.hiB = prev_hi;
                 hi_now = run ? hi : -1;
             }
-            if (run)
+            if (!BAND && c > 0) {
+                if constexpr (!BAND)
+                    m = g1_strip<MODE, FMT, false, QN, false, true>(a, Q, A, B, qwA, qwB, c * G1_R, c * G1_R, rd, rd,
+                                                                    last ? -1 : wr, false, 0u, dummy, st, sc, twc, bd);
+            } else if (run) {
                 m = g1_strip<MODE, FMT, false, QN, BAND>(a, Q, A, B, qwA, qwB, c * G1_R, c * G1_R, rd, rd,
-                                                         last ? -1 : wr, BAND || c == 0, 0u, dummy, st, sc, twc, bd);
+                                                         last ? -1 : wr, true, 0u, dummy, st, sc, twc, bd);
+            }
             if (c < chunks) {
                 if (lo16(m) > bestA) {
                     bestA = lo16(m);
@@ -674,13 +732,25 @@ const void* dp_g1_kernel_ptr(int mode, int fmt, bool qn, bool band) {
     return mode == SALOBA_EXTEND ? g1_ptr<1, false>(fmt, qn) : g1_ptr<0, false>(fmt, qn);
 }
 int g1_threads() { return G1_T; }
+size_t g1_smem_bytes(bool qn) { return qn ? sizeof(G1Stage<true>) : sizeof(G1Stage<false>); }
+// the stage is dynamic shared memory above the 48 KB default: opt every instance in (per device)
+void g1_set_smem_attrs() {
+    for (int mode = 0; mode < 2; ++mode)
+        for (int band = 0; band < 2; ++band)
+            for (int fmt : {int(SALOBA_PACK2), int(SALOBA_PACK4)})
+                for (int qn = 0; qn < 2; ++qn) {
+                    const bool q = qn && !band;
+                    cudaFuncSetAttribute(dp_g1_kernel_ptr(mode, fmt, q, band != 0),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(g1_smem_bytes(q)));
+                }
+}
 int64_t g1_scratch_words(int64_t qcap) { return int64_t(G1_T) * g1_words_per_block() * qcap; }
 
 void launch_dp_g1(int mode, int grid, const AlignArgs& a, int bin, bool qn, cudaStream_t s) {
     const void* fn = dp_g1_kernel_ptr(mode, a.fmt, qn, a.band_w != nullptr);
     AlignArgs args = a;
     void* params[] = {&args, &bin};
-    cudaLaunchKernel(fn, dim3(grid), dim3(G1_T), params, 0, s);
+    cudaLaunchKernel(fn, dim3(grid), dim3(G1_T), params, g1_smem_bytes(qn && a.band_w == nullptr), s);
     count_launches(1);
 }
 

@@ -85,14 +85,26 @@ struct Stage {
 #endif  // pass 1: slots 0..STAGE_DEPTH-1; pass 2: A rows 0..1, B rows 2..3
 };
 
-template <int G, int R, int MODE, int FMT, bool PASS2, bool QN = false>
+// Cooperative long-pair kernel (dp_coop_kernel below): a chunk's top row is produced by ANOTHER warp
+// of the block while this chunk runs.  `in` is the producer's progress word, `in_tag | blocks` once
+// `blocks` bottom-row blocks of the producing task are in global memory; `out` is this chunk's own.
+constexpr int COOP_PUB = 16;  // bottom-row blocks per progress publication
+struct CoopIO {
+    const volatile unsigned long long* in;
+    unsigned long long in_tag;
+    volatile unsigned long long* out;
+    unsigned long long out_tag;
+};
+
+template <int G, int R, int MODE, int FMT, bool PASS2, bool QN = false, bool COOP = false>
 __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned mask, const int k, const int Q,
                                               const HalfInfo& A, const HalfInfo& B,
                                               const uint32_t* __restrict__ twA, const uint32_t* __restrict__ twB,
                                               const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
                                               const int rowA0, const int rowB0,
                                               const ChunkIO io, const uint32_t target, int (&hit)[4], Stage<G>& st,
-                                              const int sub, const uint32_t (&twraw)[R / 4]) {
+                                              const int sub, const uint32_t (&twraw)[R / 4],
+                                              const CoopIO cio = CoopIO{}) {
     const int al = a.alpha, be = a.beta;
     const uint32_t nbeta = pack2(-be, -be), nalpha = pack2(-al, -al), noGap = pack2(-al - be, -al - be);
     const uint32_t mmw = pack2(a.mismatch, a.mismatch);  // QN: substitution of an N column
@@ -154,6 +166,7 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
     const bool topA_mem = io.topA != nullptr;
 #endif
     const bool topB_mem = PASS2 && io.topB != io.topA && io.topB != nullptr;
+    [[maybe_unused]] int avail = 0;  // COOP: top-row blocks known to be published
     auto prefetch = [&](int s2, int slot) {
         const int w2 = s2 - k;
         if (unsigned(w2) < unsigned(Q)) {
@@ -162,6 +175,15 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
             if (8 * w2 < B.n) cp_async4(&st.q[slot][1][threadIdx.x], qwB + wi);
             if (k == 0) {
                 if (topA_mem) {
+                    if constexpr (COOP) {  // block w2 of the producer's bottom row must be in memory
+                        if (w2 >= avail) {  // re-read (and fence) only past what is known published
+                            unsigned long long v;
+                            while ((v = *cio.in) < (cio.in_tag | unsigned(w2 + 1))) {
+                            }
+                            avail = v >= cio.in_tag + (1ull << 32) ? Q : int(v - cio.in_tag);
+                            __threadfence_block();
+                        }
+                    }
 #pragma unroll
                     for (int q = 0; q < 4; ++q) cp_async16(&st.top[slot][sub][q], io.topA + 16 * w2 + 4 * q);
                 }
@@ -359,6 +381,12 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
             uint4* p = reinterpret_cast<uint4*>(io.bot + 16 * w);
 #pragma unroll
             for (int q = 0; q < 4; ++q) p[q] = make_uint4(botH[2 * q], botF[2 * q], botH[2 * q + 1], botF[2 * q + 1]);
+            if constexpr (COOP) {  // publish blocks [0, w] every COOP_PUB blocks (one fence per batch)
+                if ((w + 1) % COOP_PUB == 0 || w + 1 == Q) {
+                    __threadfence_block();
+                    *cio.out = cio.out_tag | unsigned(w + 1);
+                }
+            }
         }
     }
     return vmax(vmax(M0, M1), vmax(M2, M3));
@@ -518,6 +546,284 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 * 128 / I16_THREADS : 
         }
     }
     release_block_slot(a.slot_bitmap, bslot);
+}
+
+// ---- cooperative long-pair kernel (§III-A load imbalance; §IV) ----
+// With few long pairs, one warp per pair-duo leaves the GPU waiting on its longest duos: a duo of
+// 10 kbp reads is ~20 chunks of 512 rows that one warp runs one after another.  Here a block of
+// COOP_W warps shares each duo: chunk c runs on warp c % COOP_W as soon as chunk c-1 (on the
+// previous warp) has published the first blocks of its bottom row, so COOP_W chunks of the same duo
+// are in flight, staggered, each a G = 32 wavefront (run_chunk).  Per block the work is a stream
+// of TASKS: for each duo taken from the long bin, its chunks 0..C-1, then one pass-2 task; task t
+// runs on warp t % COOP_W.  Pass 2 of one duo therefore overlaps the chunks of the next one.
+//   * chunk-boundary rows live in the block's spill slot: task t writes row t % COOP_NROW (COOP_NROW =
+//     COOP_W + 1: the next writer of that row is task t + COOP_NROW, which runs on the same warp as the
+//     row's only reader, task t + 1, and after it);
+//   * progress words (one per warp, (task << 32) | blocks written) order a chunk's reads of its top row
+//     after the producer's writes (fence.cta on both sides);
+//   * the tie rule needs the running maximum in CHUNK order: a chunk's bookkeeping waits for its
+//     predecessor's, and a chunk that raises a half's maximum copies its top row (still intact: its
+//     next writer runs on this warp, later) to that half's checkpoint row for pass 2.
+// Every wait is on a task with a smaller index, and a warp runs its tasks in index order, so the
+// smallest unfinished task can always proceed (no deadlock); all warps of a block are co-resident.
+constexpr int COOP_W = I16_THREADS / 32;
+constexpr int COOP_NDUO = 4;           // duo descriptors in flight per block
+constexpr int COOP_NROW = COOP_W + 1;  // chunk-boundary rows; checkpoint rows follow (2 per descriptor)
+constexpr int COOP_GIDX = NGROUPS;     // long_gidx value that selects this kernel for the long bin
+
+struct CoopDuo {
+    int index;       // duo number n this descriptor holds (slot n % COOP_NDUO); -1 while rewritten
+    int item;        // work item (pair-duo) index in the bin, -1: the bin is exhausted
+    int t0;          // first task of the duo
+    int chunks;      // chunk tasks; the pass-2 task is t0 + chunks
+    int bestA, bestB, ckA, ckB, bufA, bufB;  // running maxima / first chunk reaching them / its top row
+    int done_chunk;  // last chunk whose bookkeeping is complete
+    int finished;    // pass 2 done and results written: the descriptor may be reused
+};
+struct CoopShared {
+    unsigned long long prog[COOP_W];
+    CoopDuo duo[COOP_NDUO];
+    int n_duos;  // descriptors published
+    int next_t;  // first task of the next duo
+    int lock;
+};
+
+__device__ __forceinline__ void coop_halves(const AlignArgs& a, int start, int cnt, int item, HalfInfo& A, HalfInfo& B) {
+    A.p = int(a.perm[start + 2 * item]);
+    B.p = 2 * item + 1 < cnt ? int(a.perm[start + 2 * item + 1]) : -1;
+    A.n = a.q_len[A.p];
+    A.m = a.t_len[A.p];
+    A.h0 = a.h0 ? a.h0[A.p] : 0;
+    B.n = B.p >= 0 ? a.q_len[B.p] : 0;
+    B.m = B.p >= 0 ? a.t_len[B.p] : 0;
+    B.h0 = (a.h0 && B.p >= 0) ? a.h0[B.p] : 0;
+}
+
+template <int MODE, int FMT>
+__global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignArgs a, int bin) {
+    constexpr int G = 32, R = 16, CH = G * R;  // rows per chunk
+    constexpr unsigned FULL = 0xffffffffu;
+    if (*a.long_gidx != COOP_GIDX) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int start = a.bin_start[bin];
+    const int cnt = a.bin_start[bin + 1] - start;
+    const int items = (cnt + 1) >> 1;
+    if (int64_t(blockIdx.x) >= int64_t(items)) return;
+    const int bslot = acquire_block_slot(a.slot_bitmap, a.slot_words);
+    const int64_t S = a.spill_stride;
+    uint32_t* const pool = reinterpret_cast<uint32_t*>(a.spill) + bslot * a.block_slot_words;
+    auto row = [&](int r) { return pool + int64_t(r) * 2 * S; };
+    __shared__ Stage<G> st;
+    __shared__ CoopShared cs;
+    if (threadIdx.x == 0) {
+        cs.n_duos = 0;
+        cs.next_t = 0;
+        cs.lock = 0;
+        for (int i = 0; i < COOP_NDUO; ++i) {
+            cs.duo[i].finished = 1;
+            cs.duo[i].index = -1;
+        }
+    }
+    if (threadIdx.x < COOP_W) cs.prog[threadIdx.x] = 0;
+    __syncthreads();
+    volatile CoopShared& vs = cs;
+
+    int n = 0;  // duo of this warp's current task (descriptors are published in task order)
+    for (int t = warp;; t += COOP_W) {
+        // ---- the descriptor holding task t (lane 0 finds it, publishing new ones under the block
+        // lock; the result is broadcast so the warp stays uniform) ----
+        int item = -1, t0 = 0, chunks = 0;
+        if (lane == 0) {
+            for (;;) {
+                if (n >= vs.n_duos) {
+                    while (atomicCAS(&cs.lock, 0, 1) != 0) {
+                    }
+                    __threadfence_block();
+                    while (vs.n_duos <= n) {
+                        const int slot = vs.n_duos % COOP_NDUO;
+                        while (!vs.duo[slot].finished) {  // descriptor n_duos - COOP_NDUO still in use
+                        }
+                        const int it = atomicAdd(a.bin_counter + bin, 1);
+                        int ch = 0;
+                        HalfInfo A{}, B{};
+                        if (it < items) {
+                            coop_halves(a, start, cnt, it, A, B);
+                            ch = max((A.m + CH - 1) / CH, (B.m + CH - 1) / CH);
+                        }
+                        volatile CoopDuo& d = vs.duo[slot];
+                        d.index = -1;
+                        __threadfence_block();
+                        d.item = it < items ? it : -1;
+                        d.t0 = vs.next_t;
+                        d.chunks = ch;
+                        d.bestA = MODE ? A.h0 : 0;  // the floors (strict improvement records a chunk)
+                        d.bestB = MODE ? B.h0 : 0;
+                        d.ckA = d.ckB = d.bufA = d.bufB = -1;
+                        d.done_chunk = -1;
+                        d.finished = it < items ? 0 : 1;
+                        vs.next_t = it < items ? vs.next_t + ch + 1 : INT_MAX;
+                        __threadfence_block();
+                        d.index = vs.n_duos;
+                        __threadfence_block();
+                        vs.n_duos = vs.n_duos + 1;
+                    }
+                    __threadfence_block();
+                    atomicExch(&cs.lock, 0);
+                }
+                // A descriptor no longer holding duo n means duo n finished and its slot was reused:
+                // this warp's (unfinished) task is in a later duo.  Fields are read between two reads
+                // of `index` (the publisher invalidates it first and sets it last).
+                const volatile CoopDuo& d = vs.duo[n % COOP_NDUO];
+                const int i1 = d.index;
+                __threadfence_block();
+                item = d.item;
+                t0 = d.t0;
+                chunks = d.chunks;
+                __threadfence_block();
+                const int i2 = d.index;
+                if (i1 == n && i2 == n && (item < 0 || t <= t0 + chunks)) break;
+                ++n;
+            }
+        }
+        n = __shfl_sync(FULL, n, 0);
+        item = __shfl_sync(FULL, item, 0);
+        t0 = __shfl_sync(FULL, t0, 0);
+        chunks = __shfl_sync(FULL, chunks, 0);
+        __syncwarp(FULL);
+        if (item < 0) break;  // the bin is exhausted
+        volatile CoopDuo& d = vs.duo[n % COOP_NDUO];
+        HalfInfo A, B;
+        coop_halves(a, start, cnt, item, A, B);
+        if (!MODE) A.h0 = B.h0 = 0;
+        const uint32_t* qwA = a.q_words + a.q_word_off[A.p];
+        const uint32_t* twA = a.t_words + a.t_word_off[A.p];
+        const uint32_t* qwB = B.p >= 0 ? a.q_words + a.q_word_off[B.p] : qwA;
+        const uint32_t* twB = B.p >= 0 ? a.t_words + a.t_word_off[B.p] : twA;
+        const int Q = (max(A.n, B.n) + 7) >> 3;
+        const int c = t - t0;
+        if (c < chunks) {
+            // ---- chunk task ----
+            ChunkIO io;
+            io.topA = io.topB = c > 0 ? row((t - 1) % COOP_NROW) : nullptr;
+            io.bot = c + 1 < chunks ? row(t % COOP_NROW) : nullptr;
+            const CoopIO cio{&cs.prog[(t - 1 + COOP_W) % COOP_W], (unsigned long long)(t - 1) << 32, &cs.prog[warp],
+                             (unsigned long long)t << 32};
+            uint32_t tw[R / 4];
+            load_target_raw<R, FMT>(A, B, twA, twB, c * CH + R * lane, c * CH + R * lane, tw);
+            int dummy[4];
+            uint32_t m = run_chunk<G, R, MODE, FMT, false, false, true>(a, FULL, lane, Q, A, B, twA, twB, qwA, qwB,
+                                                                        c * CH, c * CH, io, 0u, dummy, st, warp, tw, cio);
+#pragma unroll
+            for (int off = 1; off < G; off <<= 1) m = vmax(m, __shfl_xor_sync(FULL, m, off));
+            // bookkeeping in chunk order (strict improvement keeps the first chunk reaching a maximum)
+            int upd = 0;
+            if (lane == 0) {
+                while (d.done_chunk != c - 1) {
+                }
+                __threadfence_block();
+                const int bA = d.bestA, bB = d.bestB;
+                upd = (lo16(m) > bA ? 1 : 0) | (B.p >= 0 && hi16(m) > bB ? 2 : 0);
+                d.bestA = max(bA, lo16(m));
+                d.bestB = max(bB, hi16(m));
+            }
+            upd = __shfl_sync(FULL, upd, 0);
+            const int slot = n % COOP_NDUO;
+            for (int h = 0; h < 2; ++h) {
+                if (!(upd & (1 << h))) continue;
+                const int ck = COOP_NROW + 2 * slot + h;
+                if (c > 0) {  // this chunk's top row becomes the half's checkpoint
+                    const uint4* src = reinterpret_cast<const uint4*>(row((t - 1) % COOP_NROW));
+                    uint4* dst = reinterpret_cast<uint4*>(row(ck));
+                    for (int i = lane; i < 4 * Q; i += 32) dst[i] = __ldcg(src + i);
+                }
+                if (lane == 0) {
+                    if (h == 0) {
+                        d.ckA = c;
+                        d.bufA = c > 0 ? ck : -1;
+                    } else {
+                        d.ckB = c;
+                        d.bufB = c > 0 ? ck : -1;
+                    }
+                }
+            }
+            __syncwarp(FULL);
+            if (lane == 0) {
+                __threadfence_block();
+                d.done_chunk = c;
+            }
+            __syncwarp(FULL);
+        } else {
+            // ---- pass-2 task: the first cell (row-major) equal to each half's maximum ----
+            int ckA = 0, ckB = 0, bestA = 0, bestB = 0, bufA = 0, bufB = 0;
+            if (lane == 0) {
+                while (d.done_chunk != chunks - 1) {
+                }
+                __threadfence_block();
+                ckA = d.ckA, ckB = d.ckB, bestA = d.bestA, bestB = d.bestB, bufA = d.bufA, bufB = d.bufB;
+            }
+            ckA = __shfl_sync(FULL, ckA, 0);
+            ckB = __shfl_sync(FULL, ckB, 0);
+            bestA = __shfl_sync(FULL, bestA, 0);
+            bestB = __shfl_sync(FULL, bestB, 0);
+            bufA = __shfl_sync(FULL, bufA, 0);
+            bufB = __shfl_sync(FULL, bufB, 0);
+            int hit[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
+            if (ckA >= 0 || ckB >= 0) {
+                const int cA = ckA >= 0 ? ckA : ckB, cB = ckB >= 0 ? ckB : cA;
+                const int bA = ckA >= 0 ? bufA : bufB, bB = ckB >= 0 ? bufB : bA;
+                ChunkIO io;
+                io.topA = bA >= 0 ? row(bA) : nullptr;
+                io.topB = bB >= 0 ? row(bB) : nullptr;
+                io.bot = nullptr;
+                const uint32_t target = pack2(ckA >= 0 ? bestA : 0x7FFF, ckB >= 0 ? bestB : 0x7FFF);
+                uint32_t tw2[R / 4];
+                load_target_raw<R, FMT>(A, B, twA, twB, cA * CH + R * lane, cB * CH + R * lane, tw2);
+                run_chunk<G, R, MODE, FMT, true>(a, FULL, lane, Q, A, B, twA, twB, qwA, qwB, cA * CH, cB * CH, io, target,
+                                                 hit, st, warp, tw2);
+#pragma unroll
+                for (int off = 1; off < G; off <<= 1) {
+                    const int r0 = __shfl_xor_sync(FULL, hit[0], off), c0 = __shfl_xor_sync(FULL, hit[1], off);
+                    const int r1 = __shfl_xor_sync(FULL, hit[2], off), c1 = __shfl_xor_sync(FULL, hit[3], off);
+                    if (r0 < hit[0] || (r0 == hit[0] && c0 < hit[1])) {
+                        hit[0] = r0;
+                        hit[1] = c0;
+                    }
+                    if (r1 < hit[2] || (r1 == hit[2] && c1 < hit[3])) {
+                        hit[2] = r1;
+                        hit[3] = c1;
+                    }
+                }
+            }
+            if (lane == 0) {
+                const int z = MODE ? -1 : 0;
+                a.score[A.p] = bestA;
+                a.t_end[A.p] = ckA >= 0 ? (hit[0] == INT_MAX ? -3 : hit[0]) : z;
+                a.q_end[A.p] = ckA >= 0 ? (hit[1] == INT_MAX ? -3 : hit[1]) : z;
+                if (B.p >= 0) {
+                    a.score[B.p] = bestB;
+                    a.t_end[B.p] = ckB >= 0 ? (hit[2] == INT_MAX ? -3 : hit[2]) : z;
+                    a.q_end[B.p] = ckB >= 0 ? (hit[3] == INT_MAX ? -3 : hit[3]) : z;
+                }
+                __threadfence_block();
+                d.finished = 1;
+            }
+            __syncwarp(FULL);
+        }
+    }
+    release_block_slot(a.slot_bitmap, bslot);
+}
+
+const void* dp_coop_kernel_ptr(int mode, int fmt) {
+    if (mode == SALOBA_EXTEND) return fmt == SALOBA_PACK2 ? (const void*)dp_coop_kernel<1, 2> : (const void*)dp_coop_kernel<1, 4>;
+    return fmt == SALOBA_PACK2 ? (const void*)dp_coop_kernel<0, 2> : (const void*)dp_coop_kernel<0, 4>;
+}
+void launch_dp_coop(int mode, int grid, const AlignArgs& a, cudaStream_t s) {
+    const void* fn = dp_coop_kernel_ptr(mode, a.fmt);
+    AlignArgs args = a;
+    int bin = LONG_BIN;
+    void* params[] = {&args, &bin};
+    cudaLaunchKernel(fn, dim3(grid), dim3(I16_THREADS), params, 0, s);
+    count_launches(1);
 }
 
 template <int MODE, int FMT, int R>

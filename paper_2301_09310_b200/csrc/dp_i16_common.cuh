@@ -72,6 +72,25 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
 }
+// the same copies to a 32-bit shared-space address (computed once per strip: no per-step
+// generic-to-shared conversion, whose S2UR of the CTA id was a per-step stall in ncu)
+__device__ __forceinline__ void cp_async16s(uint32_t s, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4s(uint32_t s, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void st_global16(void* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+// base + i * stride (bytes) as one mad.wide: a 32-bit index into a 64-bit pointer without the
+// 64-bit add chain (signed: banded strips address rows relative to a base step and may step below it)
+template <typename T>
+__device__ __forceinline__ T* wide_at(T* base, int32_t i, uint32_t stride_bytes) {
+    uint64_t r;
+    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(i), "r"(stride_bytes), "l"(reinterpret_cast<uint64_t>(base)));
+    return reinterpret_cast<T*>(r);
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }

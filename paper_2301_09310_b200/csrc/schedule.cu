@@ -177,8 +177,10 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassifyArgs a) {
 // (config 5: 8,950 long pairs among 10M short ones) those long items finish last and G=32 wins
 // (4.85 vs 4.16 TCUPS).  Rule: G=16 iff the bin fills >= 4 waves of G=16 subwarps and every query
 // fits G=16's spill stride.  cap16 = pairs one G=16 wave holds (2 per subwarp).
+// A long bin of fewer than `coop_pairs` pairs (too few duos to keep every SM busy until the longest
+// one ends) runs on the cooperative kernel instead (long_gidx = NGROUPS, dp_coop_kernel in dp_i16.cu).
 __global__ void bin_scan_kernel(const int32_t* count, int32_t* start, const int32_t* long_qmax, int32_t* long_gidx,
-                                int64_t cap16, int force_gidx) {
+                                int64_t cap16, int force_gidx, int64_t coop_pairs) {
     if (threadIdx.x == 0) {
         int acc = 0;
         for (int b = 0; b < NBINS; ++b) {
@@ -187,7 +189,8 @@ __global__ void bin_scan_kernel(const int32_t* count, int32_t* start, const int3
         }
         start[NBINS] = acc;
         const bool g16 = force_gidx < 0 && int64_t(count[LONG_BIN]) >= 4 * cap16 && *long_qmax <= qmax_for_gidx(NGROUPS - 2);
-        *long_gidx = g16 ? NGROUPS - 2 : NGROUPS - 1;
+        const bool coop = force_gidx < 0 && int64_t(count[LONG_BIN]) < coop_pairs;
+        *long_gidx = coop ? NGROUPS : g16 ? NGROUPS - 2 : NGROUPS - 1;
     }
 }
 
@@ -199,7 +202,7 @@ size_t cub_sort_temp_bytes(int64_t n) {
 }
 
 cudaError_t run_classify_sort(const ClassifyArgs& ca, const SortKV& kv, int32_t* bin_start, int sms,
-                              int32_t* long_gidx, int64_t cap16, cudaStream_t s) {
+                              int32_t* long_gidx, int64_t cap16, int64_t coop_pairs, cudaStream_t s) {
     if (ca.n > 0) {
         const int64_t g8 = int64_t(sms) * 8;
         const int grid = int((ca.n + 255) / 256 < g8 ? (ca.n + 255) / 256 : g8);
@@ -210,7 +213,7 @@ cudaError_t run_classify_sort(const ClassifyArgs& ca, const SortKV& kv, int32_t*
                                                         kv.vals_out, int(ca.n), 0, 32, s);
         if (e != cudaSuccess) return e;
     }
-    bin_scan_kernel<<<1, 32, 0, s>>>(ca.bin_count, bin_start, ca.long_qmax, long_gidx, cap16, ca.force_gidx);
+    bin_scan_kernel<<<1, 32, 0, s>>>(ca.bin_count, bin_start, ca.long_qmax, long_gidx, cap16, ca.force_gidx, coop_pairs);
     count_launches(1);
     return cudaGetLastError();
 }

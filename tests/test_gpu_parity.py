@@ -271,10 +271,11 @@ def test_config4_sampled(sb):
     _sample_check(sb, 4, n=2000, sample=40)
 
 
-@pytest.mark.parametrize("n_long", [2_000, 40_000])
+@pytest.mark.parametrize("n_long", [2_000, 12_000, 40_000])
 def test_long_bin_width_rule(sb, n_long):
-    """The int16x2 long bin (DESIGN.md §4 A2) runs at G=32 for a few waves of long pairs and at
-    G=16 once it holds >= 4 waves of G=16 subwarps; both widths are checked on sampled outputs."""
+    """The int16x2 long bin (DESIGN.md §4 A2) runs on the cooperative kernel below two waves of
+    one-warp duos, at G=32 for a few waves of long pairs and at G=16 once it holds >= 4 waves of
+    G=16 subwarps; every choice is checked on sampled outputs."""
     import torch
 
     b = synth.generate(4, n_long, seed=11)
@@ -283,7 +284,7 @@ def test_long_bin_width_rule(sb, n_long):
     got = gpu_align(sb, b, sb.BWA_MEM, 0, sb.Options(bin_counts=bins, long_group=lg))
     assert got[3] == -1
     assert int(bins[13].item()) > 0
-    assert int(lg.item()) == (4 if n_long >= 40_000 else 5)
+    assert int(lg.item()) == (4 if n_long >= 40_000 else 5 if n_long >= 12_000 else 6)
     rng = np.random.default_rng(n_long)
     idx = np.unique(np.concatenate([rng.choice(b.n, 24, replace=False),
                                     np.argsort(b.qlen.astype(np.int64) * b.tlen)[-4:]]))
