@@ -484,7 +484,9 @@ def align(q_ascii, q_off, t_ascii, t_off, h0=None, scoring: Scoring = BWA_MEM, m
 def align_host(batch, scoring: Scoring = BWA_MEM, mode: int = LOCAL, options: Options | None = None,
                out=None, stream=None, ctx: "HostContext | None" = None):
     """End-to-end from host buffers (numpy / pinned CPU tensors): returns numpy-like int32 arrays
-    (score, q_end, t_end) and the host status (-1 or first bad pair)."""
+    (score, q_end, t_end) and the host status (-1 or first bad pair).  The library pipelines the
+    upload in slices; copies overlap compute only for page-locked (pinned) host memory, so the
+    default `out` is pinned (pass pinned inputs too, e.g. torch tensors with pin_memory=True)."""
     import numpy as np
 
     def host_ptr(a):
@@ -495,7 +497,7 @@ def align_host(batch, scoring: Scoring = BWA_MEM, mode: int = LOCAL, options: Op
 
     n = len(batch.q_off) - 1
     if out is None:
-        out = np.empty((3, max(n, 1)), np.int32)
+        out = torch.empty((3, max(n, 1)), dtype=torch.int32, pin_memory=torch.cuda.is_available()).numpy()
     st = ctypes.c_int64(0)
     opt = ctypes.byref(options._c()) if options is not None else None
     qo = np.ascontiguousarray(batch.q_off, np.int64)

@@ -384,13 +384,14 @@ static int align_batch_impl(const uint32_t* q_words, const int64_t* q_word_off, 
                 cudaStream_t as = aux[j % NAUX];
                 a.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(g), Qsup) + 8;
                 if (path == PATH_I16 && path * 8 + g == LONG_BIN) {
-                    // the long bin is launched at both widths; the one not chosen exits at once
+                    // the long bin: the cooperative kernel first (its blocks must be resident before
+                    // the short bins' persistent kernels take the slots: it holds the critical path),
+                    // then the one-warp kernel at both widths; the ones not chosen exit at once
+                    if (i16_rows == 16) launch_dp_coop(int(mode), d->sms * d->blocks_coop[int(mode)], a, as);
                     launch_dp_i16(int(mode), g, grid_for(d, int(mode), path, g, i16_rows), a, LONG_BIN, as);
                     AlignArgs a16 = a;
                     a16.spill_stride = 8 * std::min<int64_t>(qmax_for_gidx(g - 1), Qsup) + 8;
                     launch_dp_i16(int(mode), g - 1, grid_for(d, int(mode), path, g - 1, i16_rows), a16, LONG_BIN, as);
-                    // ... and the cooperative kernel (the long bin's spill stride of G = 32)
-                    if (i16_rows == 16) launch_dp_coop(int(mode), d->sms * d->blocks_coop[int(mode)], a, as);
                 } else if (path == PATH_I16 && g == 0 && use_g1(i16_rows)) {
                     AlignArgs a1 = a;
                     a1.spill_stride = std::min<int64_t>(qmax_for_gidx(0), Qsup);  // dp_g1: query-block capacity

@@ -122,6 +122,7 @@ struct AlignArgs {
     unsigned long long* counters;  // NEXT-4 instrumentation (saloba_options.counters) or nullptr
 };
 
+
 // NEXT-4 counters: a warp-wide sum of each lane's contribution, one atomic per counter per warp
 __device__ __forceinline__ void count_warp(unsigned long long* ctr, int idx, unsigned long long v) {
     unsigned long long t = v;

@@ -89,6 +89,7 @@ struct Stage {
 // of the block while this chunk runs.  `in` is the producer's progress word, `in_tag | blocks` once
 // `blocks` bottom-row blocks of the producing task are in global memory; `out` is this chunk's own.
 constexpr int COOP_PUB = 16;  // bottom-row blocks per progress publication
+constexpr int COOP_LAG = 48;  // extra blocks a chunk waits for before its first step
 struct CoopIO {
     const volatile unsigned long long* in;
     unsigned long long in_tag;
@@ -177,8 +178,14 @@ __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned
                 if (topA_mem) {
                     if constexpr (COOP) {  // block w2 of the producer's bottom row must be in memory
                         if (w2 >= avail) {  // re-read (and fence) only past what is known published
+                            // the first wait of a chunk also asks for COOP_LAG blocks of slack, so
+                            // the consumer does not trail its producer by less than one batch
+                            const int need = min(Q, w2 + 1 + (avail == 0 ? COOP_LAG : 0));
                             unsigned long long v;
-                            while ((v = *cio.in) < (cio.in_tag | unsigned(w2 + 1))) {
+                            unsigned ns = 32;
+                            while ((v = *cio.in) < (cio.in_tag | unsigned(need))) {
+                                __nanosleep(ns);  // a sleeping warp leaves its issue slots to the others
+                                ns = min(ns * 2, 1024u);
                             }
                             avail = v >= cio.in_tag + (1ull << 32) ? Q : int(v - cio.in_tag);
                             __threadfence_block();
@@ -636,13 +643,11 @@ __global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignA
         if (lane == 0) {
             for (;;) {
                 if (n >= vs.n_duos) {
-                    while (atomicCAS(&cs.lock, 0, 1) != 0) {
-                    }
+                    while (atomicCAS(&cs.lock, 0, 1) != 0) __nanosleep(64);
                     __threadfence_block();
                     while (vs.n_duos <= n) {
                         const int slot = vs.n_duos % COOP_NDUO;
-                        while (!vs.duo[slot].finished) {  // descriptor n_duos - COOP_NDUO still in use
-                        }
+                        while (!vs.duo[slot].finished) __nanosleep(256);  // duo n_duos - COOP_NDUO still in use
                         const int it = atomicAdd(a.bin_counter + bin, 1);
                         int ch = 0;
                         HalfInfo A{}, B{};
@@ -718,8 +723,7 @@ __global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignA
             // bookkeeping in chunk order (strict improvement keeps the first chunk reaching a maximum)
             int upd = 0;
             if (lane == 0) {
-                while (d.done_chunk != c - 1) {
-                }
+                while (d.done_chunk != c - 1) __nanosleep(128);
                 __threadfence_block();
                 const int bA = d.bestA, bB = d.bestB;
                 upd = (lo16(m) > bA ? 1 : 0) | (B.p >= 0 && hi16(m) > bB ? 2 : 0);
@@ -756,8 +760,7 @@ __global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignA
             // ---- pass-2 task: the first cell (row-major) equal to each half's maximum ----
             int ckA = 0, ckB = 0, bestA = 0, bestB = 0, bufA = 0, bufB = 0;
             if (lane == 0) {
-                while (d.done_chunk != chunks - 1) {
-                }
+                while (d.done_chunk != chunks - 1) __nanosleep(256);
                 __threadfence_block();
                 ckA = d.ckA, ckB = d.ckB, bestA = d.bestA, bestB = d.bestB, bufA = d.bufA, bufB = d.bufB;
             }
