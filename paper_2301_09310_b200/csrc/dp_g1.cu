@@ -54,6 +54,9 @@ __host__ __device__ constexpr int g1_depth() { return QN && G1_DEPTH > 3 ? 3 : G
 #ifndef G1_ROLL
 #define G1_ROLL 1
 #endif
+#ifndef G1_CW2
+#define G1_CW2 4  // columns per rolled iteration of the compact pass-2 body
+#endif
 #ifndef G1_DEPTH2_CFG
 #define G1_DEPTH2_CFG 2
 #endif
@@ -125,15 +128,36 @@ __device__ __forceinline__ uint32_t band_bits(int d, int w) {
     return lo > hi ? 0u : ((2u << hi) - 1u) & ~((1u << lo) - 1u);
 }
 
+// The step's 8 PRMT selectors from the two packed query words (QN: N flags in bytes 2 / 3 of each
+// selector word for half A / B; PRMT reads only the low 16 bits, the compute loop expands them).
+template <int FMT, bool QN>
+__device__ __forceinline__ void g1_selectors(uint32_t qwordA, uint32_t qwordB, int s, const HalfInfo& A,
+                                             const HalfInfo& B, uint32_t (&sel)[8]) {
+    const uint32_t qcA = staged_codes<FMT>(qwordA, s, A.n);
+    const uint32_t qcB = staged_codes<FMT>(qwordB, s, B.n);
+    make_selectors(qcA, qcB, sel);
+    if constexpr (QN) {
+        const uint32_t vA = qcA ^ 0x44444444u, vB = qcB ^ 0x44444444u;
+        const uint32_t zA = ~(((vA & 0x77777777u) + 0x77777777u) | vA) & 0x88888888u;
+        const uint32_t zB = ~(((vB & 0x77777777u) + 0x77777777u) | vB) & 0x88888888u;
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+            sel[x] = (sel[x] & 0xFFFFu) | (((zA >> (4 * x + 3)) & 1u) * 0x00FF0000u) |
+                     (((zB >> (4 * x + 3)) & 1u) * 0xFF000000u);
+    }
+}
+
 // One 16-row strip of both halves.
 //   PASS2 = false: returns the lane's maximum of the diagonal candidates D over the strip (max H =
 //     max(0, max D): a positive H reached through a gap is strictly below an earlier cell).
 //   PASS2 = true: records the first cell (row-major) equal to `target` per half into hit[].
-//   selgen: build the selectors from the query words and store them (chunk 0 of pass 1).
+//   selgen: build the selectors from the query words every step (banded strips; unbanded items get
+//     theirs from the prologue's scratch).
 //   topA / topB: spill buffer of the top row per half (-1: the table boundary); bot: buffer that
 //     receives the bottom row (-1: none).
-//   HOT: pass 1 below chunk 0 without a band (the bulk of the work): compile-time selgen = false and
-//     top row from the spill buffer, so the step loop carries no boundary or selector-build code.
+//   HOT: pass 1 without a band (the bulk of the work; chunk 0 reads the prologue's boundary row):
+//     compile-time selgen = false and top row from memory, so the step loop carries no boundary or
+//     selector-build code.
 //   BAND: only cells |i - j| <= w (per half) are in the table; the strip runs steps
 //     [bd.s_begin, bd.s_end] (a corner visit + the union of the warp's band blocks), blocks that
 //     cross a band edge mask their out-of-band cells to H = E = F = 0, selectors are built every
@@ -311,30 +335,8 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
             dpk = pack2(min(max(rA - 8 * s, -16000), 16000), min(max(rB - 8 * s, -16000), 16000));
         }
         uint32_t sel[8];
-        if (selgen) {
-            const uint32_t qcA = staged_codes<FMT>(nq0, s, A.n);
-            const uint32_t qcB = staged_codes<FMT>(nq1, s, B.n);
-            make_selectors(qcA, qcB, sel);
-            if constexpr (QN) {
-                // N columns (nibble 4): bytes 2 / 3 of the selector word set to 0xFF for half A / B;
-                // PRMT reads only the low 16 bits, the compute loop expands the flags to masks
-                const uint32_t vA = qcA ^ 0x44444444u, vB = qcB ^ 0x44444444u;
-                const uint32_t zA = ~(((vA & 0x77777777u) + 0x77777777u) | vA) & 0x88888888u;
-                const uint32_t zB = ~(((vB & 0x77777777u) + 0x77777777u) | vB) & 0x88888888u;
-#pragma unroll
-                for (int x = 0; x < 8; ++x)
-                    sel[x] = (sel[x] & 0xFFFFu) | (((zA >> (4 * x + 3)) & 1u) * 0x00FF0000u) |
-                             (((zB >> (4 * x + 3)) & 1u) * 0xFF000000u);
-            }
-            if (BAND) {
-                // banded strips build selectors every step (no selector scratch)
-            } else if (QN) {
-                *sc.sel_at(s, 0) = make_uint4(sel[0], sel[1], sel[2], sel[3]);
-                *sc.sel_at(s, 1) = make_uint4(sel[4], sel[5], sel[6], sel[7]);
-            } else {  // compact: two 16-bit selectors per word (PRMT reads only the low 16 bits)
-                *sc.sel_at(s, 0) = make_uint4(prmt(sel[0], sel[1], 0x5410), prmt(sel[2], sel[3], 0x5410),
-                                              prmt(sel[4], sel[5], 0x5410), prmt(sel[6], sel[7], 0x5410));
-            }
+        if (selgen) {  // banded strips build their selectors every step (no selector scratch)
+            g1_selectors<FMT, QN>(nq0, nq1, s, A, B, sel);
         } else if (QN) {
             sel[0] = nsel0.x; sel[1] = nsel0.y; sel[2] = nsel0.z; sel[3] = nsel0.w;
             sel[4] = nsel1.x; sel[5] = nsel1.y; sel[6] = nsel1.z; sel[7] = nsel1.w;
@@ -441,32 +443,40 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
         // pass-1 loop (chunk 0, pass 2; G1_ROLL): their steps are 1/8 of the work, and a second and
         // third fully unrolled body made the kernel's hot code outgrow the instruction cache (ncu:
         // no-instruction stalls at every branch of pass 2's unrolled body)
-        auto edge_body = [&](auto mask_tag) {
+        // CW columns per rolled iteration (2 or 4): more columns, more independent chains in flight
+        auto edge_body = [&](auto mask_tag, auto cw_tag) {
             constexpr bool MASK = decltype(mask_tag)::value;
+            constexpr int CW = decltype(cw_tag)::value, NPI = CW / 2;
             const uint32_t wbA = MASK ? band_bits(rA - 8 * s, int(bd.wpk & 0xFFFFu)) : 0u;
             const uint32_t wbB = MASK ? band_bits(rB - 8 * s, int(bd.wpk >> 16)) : 0u;
             uint32_t hdiag_top = corner;
 #pragma unroll 1
-            for (int p = 0; p < 4; ++p) {
-                const uint4 tqp = TOP(slot, p);
-                uint4 tbp = tqp;
-                if (PASS2 && split) tbp = TOP(BOFF + slot, p);
-                uint32_t se = sel[0], so = sel[1];
+            for (int p = 0; p < 8 / CW; ++p) {
+                uint4 tq[NPI], tb[NPI];
 #pragma unroll
-                for (int k = 1; k < 4; ++k) {
-                    se = p == k ? sel[2 * k] : se;
-                    so = p == k ? sel[2 * k + 1] : so;
+                for (int i = 0; i < NPI; ++i) {
+                    tq[i] = TOP(slot, NPI * p + i);
+                    tb[i] = tq[i];
+                    if (PASS2 && split) tb[i] = TOP(BOFF + slot, NPI * p + i);
                 }
-                uint32_t bh[2], bf[2];
+                uint32_t sx[CW];
 #pragma unroll
-                for (int xx = 0; xx < 2; ++xx) {
-                    const int x = 2 * p + xx;
-                    uint32_t hup = xx ? tqp.z : tqp.x, fup = xx ? tqp.w : tqp.y;
+                for (int xx = 0; xx < CW; ++xx) {
+                    sx[xx] = sel[xx];
+#pragma unroll
+                    for (int k = 1; k < 8 / CW; ++k) sx[xx] = p == k ? sel[CW * k + xx] : sx[xx];
+                }
+                uint32_t bh[CW], bf[CW];
+#pragma unroll
+                for (int xx = 0; xx < CW; ++xx) {
+                    const int x = CW * p + xx;
+                    const uint4 tqp = tq[xx >> 1], tbp = tb[xx >> 1];
+                    uint32_t hup = (xx & 1) ? tqp.z : tqp.x, fup = (xx & 1) ? tqp.w : tqp.y;
                     if (PASS2 && split) {
-                        hup = prmt(hup, xx ? tbp.z : tbp.x, 0x7610);
-                        fup = prmt(fup, xx ? tbp.w : tbp.y, 0x7610);
+                        hup = prmt(hup, (xx & 1) ? tbp.z : tbp.x, 0x7610);
+                        fup = prmt(fup, (xx & 1) ? tbp.w : tbp.y, 0x7610);
                     }
-                    const uint32_t selx = xx ? so : se;
+                    const uint32_t selx = sx[xx];
                     // in-band rows of column x: bit r (half A) / bit 16 + r (half B)
                     const uint32_t m = MASK ? prmt(wbA >> (7 - x), wbB >> (7 - x), 0x5410) : 0u;
                     [[maybe_unused]] uint32_t nm = 0;
@@ -515,14 +525,19 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                         }
                     }
                 }
-                if (bot >= 0) st_global16(wide_at(g_bot, s - bd.wbase, str64) + p, make_uint4(bh[0], bf[0], bh[1], bf[1]));
+                if (bot >= 0) {
+#pragma unroll
+                    for (int i = 0; i < NPI; ++i)
+                        st_global16(wide_at(g_bot, s - bd.wbase, str64) + NPI * p + i,
+                                    make_uint4(bh[2 * i], bf[2 * i], bh[2 * i + 1], bf[2 * i + 1]));
+                }
             }
             corner = hdiag_top;
         };
         if (BAND && edge) {
-            edge_body(std::true_type{});
+            edge_body(std::true_type{}, std::integral_constant<int, 2>{});
         } else if (!HOT && !BAND && G1_ROLL) {
-            edge_body(std::false_type{});
+            edge_body(std::false_type{}, std::integral_constant<int, G1_CW2>{});
         } else {
             step_body(std::false_type{});
             if (bot >= 0) {
@@ -533,6 +548,40 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
         }
     }
     return vmax(vmax(M0, M1), vmax(M2, M3));
+}
+
+// Unbanded items, before pass 1: every query block's selectors into the thread's scratch, and the
+// table-boundary top row H(-1, j), F(-1, j) into spill buffer `buf`, so that chunk 0 runs the same
+// hot strip as every other chunk (it used to build both per step in a slower generic strip: ncu,
+// 1/16 of the steps took 8.6% of the kernel's samples).
+template <int MODE, int FMT, bool QN>
+__device__ __forceinline__ void g1_prologue(const AlignArgs& a, int Q, const HalfInfo& A, const HalfInfo& B,
+                                            const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
+                                            const G1Scratch& sc, int buf) {
+    const int al = a.alpha, be = a.beta;
+    const uint32_t noGap = pack2(-al - be, -al - be);
+#pragma unroll 4
+    for (int s = 0; s < Q; ++s) {
+        const int wi = FMT == SALOBA_PACK2 ? (s >> 1) : s;
+        const uint32_t qa = 8 * s < A.n ? __ldg(qwA + wi) : 0u, qb = 8 * s < B.n ? __ldg(qwB + wi) : 0u;
+        uint32_t sel[8];
+        g1_selectors<FMT, QN>(qa, qb, s, A, B, sel);
+        if (QN) {
+            st_global16(sc.sel_at(s, 0), make_uint4(sel[0], sel[1], sel[2], sel[3]));
+            st_global16(sc.sel_at(s, 1), make_uint4(sel[4], sel[5], sel[6], sel[7]));
+        } else {  // compact: two 16-bit selectors per word (PRMT reads only the low 16 bits)
+            st_global16(sc.sel_at(s, 0), make_uint4(prmt(sel[0], sel[1], 0x5410), prmt(sel[2], sel[3], 0x5410),
+                                                    prmt(sel[4], sel[5], 0x5410), prmt(sel[6], sel[7], 0x5410)));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = 8 * s + 2 * q;
+            const uint32_t h0v = pack2(MODE ? max(0, A.h0 - al - be * j) : 0, MODE ? max(0, B.h0 - al - be * j) : 0);
+            const uint32_t h1v =
+                pack2(MODE ? max(0, A.h0 - al - be * (j + 1)) : 0, MODE ? max(0, B.h0 - al - be * (j + 1)) : 0);
+            st_global16(sc.row_at(buf, s, q), make_uint4(h0v, noGap, h1v, noGap));
+        }
+    }
 }
 
 // warp-uniform band step range of a strip starting at row r0 (both halves, union over the warp);
@@ -609,6 +658,10 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
         int ckA = -1, ckB = -1;              // chunk holding the first maximum (-1: none above floor)
         int bufA = -1, bufB = -1;            // buffer holding that chunk's top row (-1: boundary)
         int rd = -1, wr = 0;
+        if constexpr (!BAND) {
+            g1_prologue<MODE, FMT, QN>(a, Q, A, B, qwA, qwB, sc, G1_NBUF - 1);
+            rd = G1_NBUF - 1;  // chunk 0's top row: the boundary row just written
+        }
         uint32_t twn[4];
         g1_target_raw<FMT>(A, B, twA, twB, 0, 0, twn);
         for (int c = 0; c < chunks_w; ++c) {
@@ -633,7 +686,7 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
                 bd.hiA = bd.hiB = prev_hi;
                 hi_now = run ? hi : -1;
             }
-            if (!BAND && c > 0) {
+            if (!BAND) {
                 if constexpr (!BAND)
                     m = g1_strip<MODE, FMT, false, QN, false, true>(a, Q, A, B, qwA, qwB, c * G1_R, c * G1_R, rd, rd,
                                                                     last ? -1 : wr, false, 0u, dummy, st, sc, twc, bd);

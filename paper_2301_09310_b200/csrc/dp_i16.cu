@@ -561,8 +561,10 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 * 128 / I16_THREADS : 
 // COOP_W warps shares each duo: chunk c runs on warp c % COOP_W as soon as chunk c-1 (on the
 // previous warp) has published the first blocks of its bottom row, so COOP_W chunks of the same duo
 // are in flight, staggered, each a G = 32 wavefront (run_chunk).  Per block the work is a stream
-// of TASKS: for each duo taken from the long bin, its chunks 0..C-1, then one pass-2 task; task t
-// runs on warp t % COOP_W.  Pass 2 of one duo therefore overlaps the chunks of the next one.
+// of TASKS: for each duo taken from the long bin, its chunks 0..C-1, then the pass-2 task of the
+// PREVIOUS duo; task t runs on warp t % COOP_W.  A pass-2 task placed right after its own duo's
+// chunks waited up to a whole chunk for the last of them (ncu: a third of the warps asleep on
+// config 4); one duo later, its chunks are done and it overlaps the next duo's chunks.
 //   * chunk-boundary rows live in the block's spill slot: task t writes row t % COOP_NROW (COOP_NROW =
 //     COOP_W + 1: the next writer of that row is task t + COOP_NROW, which runs on the same warp as the
 //     row's only reader, task t + 1, and after it);
@@ -582,7 +584,7 @@ struct CoopDuo {
     int index;       // duo number n this descriptor holds (slot n % COOP_NDUO); -1 while rewritten
     int item;        // work item (pair-duo) index in the bin, -1: the bin is exhausted
     int t0;          // first task of the duo
-    int chunks;      // chunk tasks; the pass-2 task is t0 + chunks
+    int chunks;      // chunk tasks; task t0 + chunks is the pass 2 of the previous duo
     int bestA, bestB, ckA, ckB, bufA, bufB;  // running maxima / first chunk reaching them / its top row
     int done_chunk;  // last chunk whose bookkeeping is complete
     int finished;    // pass 2 done and results written: the descriptor may be reused
@@ -695,18 +697,25 @@ __global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignA
         t0 = __shfl_sync(FULL, t0, 0);
         chunks = __shfl_sync(FULL, chunks, 0);
         __syncwarp(FULL);
-        if (item < 0) break;  // the bin is exhausted
-        volatile CoopDuo& d = vs.duo[n % COOP_NDUO];
+        const int c = t - t0;
+        // block of descriptor n: its duo's chunk tasks, then the pass-2 task of duo n - 1 (placed after
+        // duo n's chunks, so it rarely waits for duo n - 1's last chunk); the exhausted descriptor's
+        // block is that last pass-2 task alone
+        if (item < 0 && c > chunks) break;  // the bin is exhausted
+        const bool chunk_task = c < chunks;
+        if (!chunk_task && n == 0) continue;  // (no duo before the first)
+        const int dn = chunk_task ? n : n - 1;  // the duo this task works on
+        volatile CoopDuo& d = vs.duo[dn % COOP_NDUO];
+        const int ditem = chunk_task ? item : __shfl_sync(FULL, lane == 0 ? d.item : 0, 0);
         HalfInfo A, B;
-        coop_halves(a, start, cnt, item, A, B);
+        coop_halves(a, start, cnt, ditem, A, B);
         if (!MODE) A.h0 = B.h0 = 0;
         const uint32_t* qwA = a.q_words + a.q_word_off[A.p];
         const uint32_t* twA = a.t_words + a.t_word_off[A.p];
         const uint32_t* qwB = B.p >= 0 ? a.q_words + a.q_word_off[B.p] : qwA;
         const uint32_t* twB = B.p >= 0 ? a.t_words + a.t_word_off[B.p] : twA;
         const int Q = (max(A.n, B.n) + 7) >> 3;
-        const int c = t - t0;
-        if (c < chunks) {
+        if (chunk_task) {
             // ---- chunk task ----
             ChunkIO io;
             io.topA = io.topB = c > 0 ? row((t - 1) % COOP_NROW) : nullptr;
@@ -731,7 +740,7 @@ __global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignA
                 d.bestB = max(bB, hi16(m));
             }
             upd = __shfl_sync(FULL, upd, 0);
-            const int slot = n % COOP_NDUO;
+            const int slot = dn % COOP_NDUO;
             for (int h = 0; h < 2; ++h) {
                 if (!(upd & (1 << h))) continue;
                 const int ck = COOP_NROW + 2 * slot + h;
@@ -760,7 +769,8 @@ __global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignA
             // ---- pass-2 task: the first cell (row-major) equal to each half's maximum ----
             int ckA = 0, ckB = 0, bestA = 0, bestB = 0, bufA = 0, bufB = 0;
             if (lane == 0) {
-                while (d.done_chunk != chunks - 1) __nanosleep(256);
+                const int dchunks = d.chunks;
+                while (d.done_chunk != dchunks - 1) __nanosleep(256);
                 __threadfence_block();
                 ckA = d.ckA, ckB = d.ckB, bestA = d.bestA, bestB = d.bestB, bufA = d.bufA, bufB = d.bufB;
             }
