@@ -54,6 +54,14 @@ __host__ __device__ constexpr int g1_depth() { return QN && G1_DEPTH > 3 ? 3 : G
 #ifndef G1_ROLL
 #define G1_ROLL 1
 #endif
+// The per-item prologue (selectors + boundary row to memory, chunk 0 on the hot strip) measured
+// +1.5% on EXTEND (config 2) and -3.5% on LOCAL, whose boundary row is constant and whose chunk 0
+// is cheaper building it in registers: 2 = EXTEND only (default), 1 = both modes, 0 = neither.
+#ifndef G1_PROLOGUE
+#define G1_PROLOGUE 2
+#endif
+template <int MODE>
+__host__ __device__ constexpr bool g1_prologue_on() { return G1_PROLOGUE == 1 || (G1_PROLOGUE == 2 && MODE == 1); }
 #ifndef G1_CW2
 #define G1_CW2 4  // columns per rolled iteration of the compact pass-2 body
 #endif
@@ -337,6 +345,15 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
         uint32_t sel[8];
         if (selgen) {  // banded strips build their selectors every step (no selector scratch)
             g1_selectors<FMT, QN>(nq0, nq1, s, A, B, sel);
+            if (!BAND && !g1_prologue_on<MODE>()) {  // chunk 0 without the prologue stores them for later chunks
+                if (QN) {
+                    *sc.sel_at(s, 0) = make_uint4(sel[0], sel[1], sel[2], sel[3]);
+                    *sc.sel_at(s, 1) = make_uint4(sel[4], sel[5], sel[6], sel[7]);
+                } else {
+                    *sc.sel_at(s, 0) = make_uint4(prmt(sel[0], sel[1], 0x5410), prmt(sel[2], sel[3], 0x5410),
+                                                  prmt(sel[4], sel[5], 0x5410), prmt(sel[6], sel[7], 0x5410));
+                }
+            }
         } else if (QN) {
             sel[0] = nsel0.x; sel[1] = nsel0.y; sel[2] = nsel0.z; sel[3] = nsel0.w;
             sel[4] = nsel1.x; sel[5] = nsel1.y; sel[6] = nsel1.z; sel[7] = nsel1.w;
@@ -550,10 +567,10 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
     return vmax(vmax(M0, M1), vmax(M2, M3));
 }
 
-// Unbanded items, before pass 1: every query block's selectors into the thread's scratch, and the
-// table-boundary top row H(-1, j), F(-1, j) into spill buffer `buf`, so that chunk 0 runs the same
-// hot strip as every other chunk (it used to build both per step in a slower generic strip: ncu,
-// 1/16 of the steps took 8.6% of the kernel's samples).
+// Unbanded EXTEND items (g1_prologue_on), before pass 1: every query block's selectors into the
+// thread's scratch, and the table-boundary top row H(-1, j), F(-1, j) into spill buffer `buf`, so
+// that chunk 0 runs the same hot strip as every other chunk instead of building both per step in
+// the compact generic strip.
 template <int MODE, int FMT, bool QN>
 __device__ __forceinline__ void g1_prologue(const AlignArgs& a, int Q, const HalfInfo& A, const HalfInfo& B,
                                             const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
@@ -658,7 +675,7 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
         int ckA = -1, ckB = -1;              // chunk holding the first maximum (-1: none above floor)
         int bufA = -1, bufB = -1;            // buffer holding that chunk's top row (-1: boundary)
         int rd = -1, wr = 0;
-        if constexpr (!BAND) {
+        if constexpr (!BAND && g1_prologue_on<MODE>()) {
             g1_prologue<MODE, FMT, QN>(a, Q, A, B, qwA, qwB, sc, G1_NBUF - 1);
             rd = G1_NBUF - 1;  // chunk 0's top row: the boundary row just written
         }
@@ -686,7 +703,7 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
                 bd.hiA = bd.hiB = prev_hi;
                 hi_now = run ? hi : -1;
             }
-            if (!BAND) {
+            if (!BAND && (g1_prologue_on<MODE>() || c > 0)) {
                 if constexpr (!BAND)
                     m = g1_strip<MODE, FMT, false, QN, false, true>(a, Q, A, B, qwA, qwB, c * G1_R, c * G1_R, rd, rd,
                                                                     last ? -1 : wr, false, 0u, dummy, st, sc, twc, bd);
