@@ -574,15 +574,19 @@ def main():
     achieved = cells_rank / (dp_ms_avg * 1e-3) / 1e9
     traffic = None
     try:  # DRAM bytes per launch of the dominant kernel from the committed ncu capture of this command
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_dp_traffic.json")))
+        tpath = os.path.join(ROOT, "profiles", "r02_dp_traffic.json")
+        if not os.path.exists(tpath):
+            tpath = os.path.join(ROOT, "profiles", "r01_dp_traffic.json")
+        tj = json.load(open(tpath))
         if tj.get("workload") == f"config{cfg}" and tj.get("pairs") == n and args.mode == "local":
             traffic = tj["traffic_bytes_per_launch"]
     except Exception:
         pass
     roof = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GCUPS",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "kernel": ("dp_i16_kernel" if path == "int16x2" else "dp_i32_kernel") +
-                      " (all bins of one call, CUDA events on the launching stream)",
+            "kernel": (("dp_g1_kernel" if bc[8] + bc[14] >= n16 / 2 else
+                        "dp_coop_kernel" if lg == 6 and bc[13] else "dp_i16_kernel") if path == "int16x2"
+                       else "dp_i32_kernel") + " (runs most pairs; achieved = all DP kernels of one call, CUDA events on the launching stream)",
             # bin 13 = the int16x2 long bin, run at G = 2^long_group (16 or 32) this call, or (6) on the
             # cooperative kernel (several warps per duo)
             "bins": {("i16_G1_queryN" if b == 14 else "i16_G2_queryN" if b == 6 else

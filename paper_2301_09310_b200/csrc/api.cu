@@ -31,6 +31,8 @@ const void* dp_g1_kernel_ptr(int mode, int fmt, bool qn, bool band);
 int g1_threads();
 const void* dp_coop_kernel_ptr(int mode, int fmt);
 void launch_dp_coop(int mode, int grid, const AlignArgs& a, cudaStream_t s);
+int coop_threads();
+int coop_rows();
 size_t g1_smem_bytes(bool qn);
 void g1_set_smem_attrs();
 int64_t g1_scratch_words(int64_t qcap);
@@ -99,7 +101,7 @@ static const DevInfo* dev_info(int device) {
         g1_set_smem_attrs();
         for (int mode = 0; mode < 2; ++mode) {
             int nb = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_coop_kernel_ptr(mode, SALOBA_PACK4), I16_THREADS, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_coop_kernel_ptr(mode, SALOBA_PACK4), coop_threads(), 0);
             d.blocks_coop[mode] = std::max(1, nb);
             d.max_blocks_per_sm = std::max(d.max_blocks_per_sm, d.blocks_coop[mode]);
         }
@@ -203,8 +205,11 @@ static int64_t block_need_words(int path, int g, int64_t Qmax) {
     const int64_t G = int64_t(1) << g;
     const int64_t q = std::min<int64_t>(qmax_for_gidx(g), Qmax);
     const int64_t generic = int64_t(threads_for(path)) / G * rows_for(path) * (8 * q + 8);
-    // G = 1 int16x2 bins: the dp_g1 kernel's selector + spill scratch (dp_g1.cu), or the generic one
-    return path == PATH_I16 && g == 0 ? std::max(generic, g1_scratch_words(q)) : generic;
+    // G = 1 int16x2 bins: the dp_g1 kernel's selector + spill scratch (dp_g1.cu), or the generic one;
+    // the long bin: also the cooperative kernel's rows (dp_coop_kernel)
+    if (path == PATH_I16 && g == 0) return std::max(generic, g1_scratch_words(q));
+    if (path == PATH_I16 && g == NGROUPS - 1) return std::max(generic, int64_t(coop_rows()) * 2 * (8 * q + 8));
+    return generic;
 }
 static int64_t block_slot_words(int64_t Qmax) {
     int64_t w = 0;

@@ -75,13 +75,13 @@ constexpr int STAGE_DEPTH = 3;
 #ifndef I16_MINB16
 #define I16_MINB16 3
 #endif
-template <int G>
+template <int G, int T = I16_THREADS>
 struct Stage {
-    uint32_t q[STAGE_DEPTH][2][I16_THREADS];
+    uint32_t q[STAGE_DEPTH][2][T];
 #ifdef SALOBA_NO_BSTAGE
-    uint4 top[STAGE_DEPTH][I16_THREADS / G][4];
+    uint4 top[STAGE_DEPTH][T / G][4];
 #else
-    uint4 top[4][I16_THREADS / G][4];  // pass 1: slots 0..STAGE_DEPTH-1; pass 2: A rows 0..1, B rows 2..3
+    uint4 top[4][T / G][4];  // pass 1: slots 0..STAGE_DEPTH-1; pass 2: A rows 0..1, B rows 2..3
 #endif  // pass 1: slots 0..STAGE_DEPTH-1; pass 2: A rows 0..1, B rows 2..3
 };
 
@@ -97,13 +97,13 @@ struct CoopIO {
     unsigned long long out_tag;
 };
 
-template <int G, int R, int MODE, int FMT, bool PASS2, bool QN = false, bool COOP = false>
+template <int G, int R, int MODE, int FMT, bool PASS2, bool QN = false, bool COOP = false, int T = I16_THREADS>
 __device__ __forceinline__ uint32_t run_chunk(const AlignArgs& a, const unsigned mask, const int k, const int Q,
                                               const HalfInfo& A, const HalfInfo& B,
                                               const uint32_t* __restrict__ twA, const uint32_t* __restrict__ twB,
                                               const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
                                               const int rowA0, const int rowB0,
-                                              const ChunkIO io, const uint32_t target, int (&hit)[4], Stage<G>& st,
+                                              const ChunkIO io, const uint32_t target, int (&hit)[4], Stage<G, T>& st,
                                               const int sub, const uint32_t (&twraw)[R / 4],
                                               const CoopIO cio = CoopIO{}) {
     const int al = a.alpha, be = a.beta;
@@ -575,8 +575,12 @@ __global__ void __launch_bounds__(I16_THREADS, R == 8 ? 4 * 128 / I16_THREADS : 
 //     next writer runs on this warp, later) to that half's checkpoint row for pass 2.
 // Every wait is on a task with a smaller index, and a warp runs its tasks in index order, so the
 // smallest unfinished task can always proceed (no deadlock); all warps of a block are co-resident.
-constexpr int COOP_W = I16_THREADS / 32;
-constexpr int COOP_NDUO = 4;           // duo descriptors in flight per block
+#ifndef COOP_WARPS
+#define COOP_WARPS 8
+#endif
+constexpr int COOP_W = COOP_WARPS;  // warps per block = chunks of one duo in flight
+constexpr int COOP_T = 32 * COOP_W;
+constexpr int COOP_NDUO = 3;           // duo descriptors in flight per block (spill slot: (COOP_W + 1 + 2 NDUO) rows)
 constexpr int COOP_NROW = COOP_W + 1;  // chunk-boundary rows; checkpoint rows follow (2 per descriptor)
 constexpr int COOP_GIDX = NGROUPS;     // long_gidx value that selects this kernel for the long bin
 
@@ -609,7 +613,7 @@ __device__ __forceinline__ void coop_halves(const AlignArgs& a, int start, int c
 }
 
 template <int MODE, int FMT>
-__global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignArgs a, int bin) {
+__global__ void __maxnreg__(168) dp_coop_kernel(AlignArgs a, int bin) {
     constexpr int G = 32, R = 16, CH = G * R;  // rows per chunk
     constexpr unsigned FULL = 0xffffffffu;
     if (*a.long_gidx != COOP_GIDX) return;
@@ -622,7 +626,7 @@ __global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignA
     const int64_t S = a.spill_stride;
     uint32_t* const pool = reinterpret_cast<uint32_t*>(a.spill) + bslot * a.block_slot_words;
     auto row = [&](int r) { return pool + int64_t(r) * 2 * S; };
-    __shared__ Stage<G> st;
+    __shared__ Stage<G, COOP_T> st;
     __shared__ CoopShared cs;
     if (threadIdx.x == 0) {
         cs.n_duos = 0;
@@ -644,8 +648,18 @@ __global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignA
         int item = -1, t0 = 0, chunks = 0;
         if (lane == 0) {
             for (;;) {
-                if (n >= vs.n_duos) {
-                    while (atomicCAS(&cs.lock, 0, 1) != 0) __nanosleep(64);
+                // Publish up to descriptor n under the lock, unless another warp does it first: a
+                // lock holder may wait (below) for an older duo's pass 2, whose warp can need a
+                // descriptor published meanwhile, so waiters must not block on the lock itself.
+                bool got = false;
+                while (n >= vs.n_duos) {
+                    if (atomicCAS(&cs.lock, 0, 1) == 0) {
+                        got = true;
+                        break;
+                    }
+                    __nanosleep(64);
+                }
+                if (got) {
                     __threadfence_block();
                     while (vs.n_duos <= n) {
                         const int slot = vs.n_duos % COOP_NDUO;
@@ -725,7 +739,7 @@ __global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignA
             uint32_t tw[R / 4];
             load_target_raw<R, FMT>(A, B, twA, twB, c * CH + R * lane, c * CH + R * lane, tw);
             int dummy[4];
-            uint32_t m = run_chunk<G, R, MODE, FMT, false, false, true>(a, FULL, lane, Q, A, B, twA, twB, qwA, qwB,
+            uint32_t m = run_chunk<G, R, MODE, FMT, false, false, true, COOP_T>(a, FULL, lane, Q, A, B, twA, twB, qwA, qwB,
                                                                         c * CH, c * CH, io, 0u, dummy, st, warp, tw, cio);
 #pragma unroll
             for (int off = 1; off < G; off <<= 1) m = vmax(m, __shfl_xor_sync(FULL, m, off));
@@ -791,7 +805,7 @@ __global__ void __launch_bounds__(I16_THREADS, I16_MINB16) dp_coop_kernel(AlignA
                 const uint32_t target = pack2(ckA >= 0 ? bestA : 0x7FFF, ckB >= 0 ? bestB : 0x7FFF);
                 uint32_t tw2[R / 4];
                 load_target_raw<R, FMT>(A, B, twA, twB, cA * CH + R * lane, cB * CH + R * lane, tw2);
-                run_chunk<G, R, MODE, FMT, true>(a, FULL, lane, Q, A, B, twA, twB, qwA, qwB, cA * CH, cB * CH, io, target,
+                run_chunk<G, R, MODE, FMT, true, false, false, COOP_T>(a, FULL, lane, Q, A, B, twA, twB, qwA, qwB, cA * CH, cB * CH, io, target,
                                                  hit, st, warp, tw2);
 #pragma unroll
                 for (int off = 1; off < G; off <<= 1) {
@@ -835,9 +849,11 @@ void launch_dp_coop(int mode, int grid, const AlignArgs& a, cudaStream_t s) {
     AlignArgs args = a;
     int bin = LONG_BIN;
     void* params[] = {&args, &bin};
-    cudaLaunchKernel(fn, dim3(grid), dim3(I16_THREADS), params, 0, s);
+    cudaLaunchKernel(fn, dim3(grid), dim3(COOP_T), params, 0, s);
     count_launches(1);
 }
+int coop_threads() { return COOP_T; }
+int coop_rows() { return COOP_NROW + 2 * COOP_NDUO; }  // spill rows (2 x spill_stride words each) per block slot
 
 template <int MODE, int FMT, int R>
 static const void* kptr16(int gidx) {

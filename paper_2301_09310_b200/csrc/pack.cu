@@ -28,11 +28,14 @@ __device__ __forceinline__ void build_lut(uint8_t* lut, int bits) {
     }
 }
 
-// 8 bytes starting at base[pos] (only bytes < total are read; others come back as 0)
+// 8 bytes starting at base[pos] (only bytes < total are read; others come back as 0).  The word
+// loads are aligned on the ADDRESS (the buffer itself need not be 4-byte aligned: a slice of a
+// larger buffer, tests/test_gpu_parity.py) and never touch bytes before base.
 __device__ __forceinline__ uint2 load8(const uint8_t* __restrict__ base, int64_t pos, int64_t total) {
-    const int64_t a = pos & ~int64_t(3);
-    const int sh = int(pos & 3) * 8;
-    if (a + 12 <= total) {
+    const int mis = int(reinterpret_cast<uintptr_t>(base + pos) & 3u);
+    const int64_t a = pos - mis;
+    const int sh = mis * 8;
+    if (a >= 0 && a + 12 <= total) {
         const uint32_t* p = reinterpret_cast<const uint32_t*>(base + a);
         const uint32_t w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2);
         return make_uint2(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh));

@@ -189,7 +189,9 @@ __global__ void bin_scan_kernel(const int32_t* count, int32_t* start, const int3
         }
         start[NBINS] = acc;
         const bool g16 = force_gidx < 0 && int64_t(count[LONG_BIN]) >= 4 * cap16 && *long_qmax <= qmax_for_gidx(NGROUPS - 2);
-        const bool coop = force_gidx < 0 && int64_t(count[LONG_BIN]) < coop_pairs;
+        // (and only for genuinely long queries: a small batch of mid-length reads lifted into the
+        // long bin by the latency floor ran 1.6x slower cooperatively, config 3 at 3k pairs)
+        const bool coop = force_gidx < 0 && int64_t(count[LONG_BIN]) < coop_pairs && *long_qmax >= LONG_Q;
         *long_gidx = coop ? NGROUPS : g16 ? NGROUPS - 2 : NGROUPS - 1;
     }
 }

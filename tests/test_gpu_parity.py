@@ -118,6 +118,56 @@ def test_pack_random_vs_host_packer(sb):
     del rng
 
 
+def _host_pack(ascii, off, fmt):
+    """Plain numpy packer (A1 layout, S:44-52): sequence s at word off[s]//B + s, codes LSB-first,
+    padding 15 (4-bit) / 0 (2-bit)."""
+    B = 8 if fmt == 4 else 16
+    code = np.full(256, 255, np.uint8)
+    for ch, c in zip(b"ACGTUacgtu", [0, 1, 2, 3, 3, 0, 1, 2, 3, 3]):
+        code[ch] = c
+    if fmt == 4:
+        code[ord("N")] = code[ord("n")] = 4
+    out = {}
+    for s in range(len(off) - 1):
+        cs = code[ascii[off[s]:off[s + 1]]].astype(np.uint32)
+        nw = (len(cs) + B - 1) // B
+        exp = np.full(nw * B, 15 if fmt == 4 else 0, np.uint32)
+        exp[:len(cs)] = cs
+        bits = 4 if fmt == 4 else 2
+        out[int(off[s] // B + s)] = (exp.reshape(nw, B) << (bits * np.arange(B, dtype=np.uint32))).sum(1).astype(np.uint32)
+    return out
+
+
+@pytest.mark.parametrize("fmt", [4, 2])
+@pytest.mark.parametrize("shift", [0, 3, 13])
+def test_pack_every_sequence_any_alignment(sb, fmt, shift):
+    """Every word of every sequence against a host packer: lengths 0-40 (more sequence ends than
+    lanes in a 512-byte window), 100-300 and 2-9 kbp, the ASCII buffer starting at an address that
+    is not 16-byte aligned, and offsets that do not start at 0 (a slice of a larger batch)."""
+    import torch
+
+    rng = np.random.default_rng(fmt * 10 + shift)
+    alpha = np.frombuffer(b"ACGTacgtUu" + (b"Nn" if fmt == 4 else b""), np.uint8)
+    lens = np.concatenate([rng.integers(0, 41, 3000), rng.integers(100, 301, 1500), rng.integers(2000, 9000, 20)])
+    rng.shuffle(lens)
+    lead = 37  # bytes before the first sequence
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64) + lead
+    ascii = rng.choice(alpha, int(off[-1])).astype(np.uint8)
+    buf = torch.zeros(len(ascii) + 64, dtype=torch.uint8, device="cuda")
+    dev = buf[shift:shift + len(ascii)]
+    dev.copy_(torch.from_numpy(ascii))
+    w, wo, ln, st = sb.pack(dev, torch.from_numpy(off).cuda(), fmt)
+    torch.cuda.synchronize()
+    assert int(st.item()) == -1
+    w = w.cpu().numpy().view(np.uint32)
+    wo = wo.cpu().numpy()
+    assert ln.cpu().tolist() == lens.tolist()
+    exp = _host_pack(ascii, off, fmt)
+    for s in range(len(lens)):
+        e = exp[int(wo[s])]
+        assert np.array_equal(w[wo[s]:wo[s] + len(e)], e), (s, lens[s])
+
+
 def test_pack_invalid_base_reported(sb):
     import torch
 
