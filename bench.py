@@ -529,7 +529,7 @@ def main():
                   "full_table_cells": cells_rank,
                   "speedup_vs_unbanded_step": round(ms_per_step / bms, 3),
                   "launches_per_call": (sb.kernel_launches() - l0) // args.band_steps,
-                  "api": "saloba_align_banded (exact int32 kernel, band-limited step ranges)"}
+                  "api": "saloba_align_banded (int16x2 G = 1 kernel with per-strip band step ranges for short reads, exact int32 kernel for long or wide-band ones)"}
 
     # ---- NEXT-1: BWA-MEM-compatible extension over the same packed batch (saloba_ksw_extend) ----
     ksw = None
