@@ -54,14 +54,19 @@ __host__ __device__ constexpr int g1_depth() { return QN && G1_DEPTH > 3 ? 3 : G
 #ifndef G1_ROLL
 #define G1_ROLL 1
 #endif
-// The per-item prologue (selectors + boundary row to memory, chunk 0 on the hot strip) measured
-// +1.5% on EXTEND (config 2) and -3.5% on LOCAL, whose boundary row is constant and whose chunk 0
-// is cheaper building it in registers: 2 = EXTEND only (default), 1 = both modes, 0 = neither.
+// The per-item prologue writes the selectors of every query block to scratch so chunk 0 runs the
+// hot strip.  EXTEND also writes its (h0-dependent) boundary top row to a spill buffer; LOCAL's
+// boundary row is constant (H = 0, F = "no gap") and is put into the stage once per strip instead.
+// Same-box A/B on config 2 (tools/sess_var.sh): EXTEND prologue +1.5% vs chunk 0 in the compact
+// generic strip; LOCAL with the boundary row in memory -3.5%, with the constant row +0.5%.
+// 3 = that (default); 2 = EXTEND only; 1 = both modes with the row in memory; 0 = neither.
 #ifndef G1_PROLOGUE
-#define G1_PROLOGUE 2
+#define G1_PROLOGUE 3
 #endif
 template <int MODE>
-__host__ __device__ constexpr bool g1_prologue_on() { return G1_PROLOGUE == 1 || (G1_PROLOGUE == 2 && MODE == 1); }
+__host__ __device__ constexpr bool g1_prologue_on() { return G1_PROLOGUE == 1 || G1_PROLOGUE == 3 || (G1_PROLOGUE == 2 && MODE == 1); }
+template <int MODE>
+__host__ __device__ constexpr bool g1_const_top() { return G1_PROLOGUE == 3 && MODE == 0; }
 #ifndef G1_CW2
 #define G1_CW2 4  // columns per rolled iteration of the compact pass-2 body
 #endif
@@ -221,7 +226,7 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
     auto TOP = [&](int slot, int q) -> uint4& { return ENT(T0 + slot * 4 + q); };
     static_assert(!HOT || (!PASS2 && !BAND), "HOT is the unbanded pass-1 strip");
     const bool selgen = HOT ? false : selgen_rt;
-    const bool topA_mem = HOT ? true : topA >= 0;
+    const bool topA_mem = (HOT && !g1_const_top<MODE>()) ? true : topA >= 0;
     const bool topB_mem = PASS2 && topB >= 0 && topB != topA;
     const bool split = PASS2 && (topB != topA || rB != rA);  // pass 2 halves at different chunks
     const int s_last = BAND ? bd.s_end : Q - 1;
@@ -266,9 +271,16 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
     // at the end of the previous step instead measured 1-4% slower on B200.)
     uint32_t nq0 = 0, nq1 = 0;
     uint4 nsel0 = make_uint4(0, 0, 0, 0), nsel1 = nsel0, ntq = nsel0, ntb = nsel0;
+    if (HOT && !topA_mem) {  // constant boundary top row (LOCAL chunk 0): every stage slot, once
+        const uint4 cb = make_uint4(0u, noGap, 0u, noGap);
+#pragma unroll
+        for (int sl = 0; sl < DEPTH; ++sl)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) TOP(sl, q) = cb;
+    }
     auto stage_in = [&](int s2, int slot) {
         cp_async_wait<DEPTH - 2>();
-        if (!topA_mem) {
+        if (!HOT && !topA_mem) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int j = 8 * s2 + 2 * q;
@@ -567,11 +579,11 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
     return vmax(vmax(M0, M1), vmax(M2, M3));
 }
 
-// Unbanded EXTEND items (g1_prologue_on), before pass 1: every query block's selectors into the
-// thread's scratch, and the table-boundary top row H(-1, j), F(-1, j) into spill buffer `buf`, so
-// that chunk 0 runs the same hot strip as every other chunk instead of building both per step in
+// Unbanded items (g1_prologue_on), before pass 1: every query block's selectors into the thread's
+// scratch and (ROW: EXTEND) the table-boundary top row H(-1, j), F(-1, j) into spill buffer `buf`,
+// so that chunk 0 runs the same hot strip as every other chunk instead of building both per step in
 // the compact generic strip.
-template <int MODE, int FMT, bool QN>
+template <int MODE, int FMT, bool QN, bool ROW = true>
 __device__ __forceinline__ void g1_prologue(const AlignArgs& a, int Q, const HalfInfo& A, const HalfInfo& B,
                                             const uint32_t* __restrict__ qwA, const uint32_t* __restrict__ qwB,
                                             const G1Scratch& sc, int buf) {
@@ -592,6 +604,7 @@ __device__ __forceinline__ void g1_prologue(const AlignArgs& a, int Q, const Hal
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
+            if (!ROW) break;
             const int j = 8 * s + 2 * q;
             const uint32_t h0v = pack2(MODE ? max(0, A.h0 - al - be * j) : 0, MODE ? max(0, B.h0 - al - be * j) : 0);
             const uint32_t h1v =
@@ -676,8 +689,8 @@ __global__ void __launch_bounds__(G1_T, G1_MINB) dp_g1_kernel(AlignArgs a, int b
         int bufA = -1, bufB = -1;            // buffer holding that chunk's top row (-1: boundary)
         int rd = -1, wr = 0;
         if constexpr (!BAND && g1_prologue_on<MODE>()) {
-            g1_prologue<MODE, FMT, QN>(a, Q, A, B, qwA, qwB, sc, G1_NBUF - 1);
-            rd = G1_NBUF - 1;  // chunk 0's top row: the boundary row just written
+            g1_prologue<MODE, FMT, QN, !g1_const_top<MODE>()>(a, Q, A, B, qwA, qwB, sc, G1_NBUF - 1);
+            if (!g1_const_top<MODE>()) rd = G1_NBUF - 1;  // chunk 0's top row: the boundary row just written
         }
         uint32_t twn[4];
         g1_target_raw<FMT>(A, B, twA, twB, 0, 0, twn);

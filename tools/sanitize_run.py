@@ -35,10 +35,13 @@ def main():
     short = synth.generate(2, 3000, seed=5)                      # G = 1 kernel (dp_g1)
     mixed = synth.generate(3, 1500, seed=6)                      # G = 1 / 2 bins
     qn = synth.generate(2, 3000, seed=7, p_n=0.01)               # query-N variant
-    longr = synth.generate(4, 12, seed=8)                        # long bin (dp_i16 G = 16/32)
+    longr = synth.generate(4, 12, seed=8)                        # long bin (cooperative kernel)
+    longm = synth.generate(4, 600, seed=9)                       # cooperative kernel, several duos per block
     for mode in (sb.LOCAL, sb.EXTEND):
         for name, b, opt in (("short", short, None), ("mixed", mixed, None), ("qn", qn, None),
-                             ("long", longr, None), ("int32", mixed, sb.Options(force_path=1)),
+                             ("long", longr, None), ("long_stream", longm, None),
+                             ("long_onewarp", longr, sb.Options(force_group=32)),
+                             ("int32", mixed, sb.Options(force_path=1)),
                              ("G4", mixed, sb.Options(force_group=4))):
             s, qe, te, st, qst, tst = sb.align(*dev(b)[:4], dev(b)[4] if mode else None, sb.BWA_MEM, mode,
                                                options=opt)
