@@ -88,8 +88,14 @@ struct Stage {
 // Cooperative long-pair kernel (dp_coop_kernel below): a chunk's top row is produced by ANOTHER warp
 // of the block while this chunk runs.  `in` is the producer's progress word, `in_tag | blocks` once
 // `blocks` bottom-row blocks of the producing task are in global memory; `out` is this chunk's own.
-constexpr int COOP_PUB = 16;  // bottom-row blocks per progress publication
-constexpr int COOP_LAG = 48;  // extra blocks a chunk waits for before its first step
+#ifndef COOP_PUB_CFG
+#define COOP_PUB_CFG 16
+#endif
+#ifndef COOP_LAG_CFG
+#define COOP_LAG_CFG 48
+#endif
+constexpr int COOP_PUB = COOP_PUB_CFG;  // bottom-row blocks per progress publication
+constexpr int COOP_LAG = COOP_LAG_CFG;  // extra blocks a chunk waits for before its first step
 struct CoopIO {
     const volatile unsigned long long* in;
     unsigned long long in_tag;
