@@ -196,189 +196,6 @@ __global__ void __launch_bounds__(256) pack_tile2_kernel(const uint8_t* __restri
     }
 }
 
-// Stream pack (round 2).  Lanes cover the batch's ASCII in 16-byte chunks aligned to the buffer
-// (one coalesced 16-byte load per lane, 512 bytes per warp "window"), convert all 16 bytes to codes
-// at once, and every packed word is emitted by the lane whose chunk holds its first byte: the word
-// is a funnel shift of that chunk's codes and the next lane's (one shuffle).  A warp walks a
-// CONTIGUOUS range of windows, so the sequence holding each window's start carries over from the
-// previous window (one binary search per warp, not per window: per-window searches made a first
-// version 4x slower than the tile kernel); inside a window each lane finds its sequence from one
-// boundary per lane (a shared-memory histogram + warp prefix sum).
-// Algorithmic bytes per base: 1 read + 1/2 (PACK4) or 1/4 (PACK2) written.
-__device__ __forceinline__ uint32_t lut_word(const uint8_t* lut, uint32_t w, uint32_t& bad, uint32_t inv) {
-    uint32_t out = 0;  // 4 bytes -> 4 nibble codes; invalid bytes flag bit c of `bad` and become `inv`
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const uint32_t code = lut[(w >> (8 * c)) & 0xFFu];
-        const bool b = code == 0xFFu;
-        bad |= (b ? 1u : 0u) << c;
-        out |= (b ? inv : code) << (4 * c);
-    }
-    return out;
-}
-
-template <int BITS>
-__global__ void __launch_bounds__(256) pack_stream_kernel(const uint8_t* __restrict__ ascii,
-                                                          const int64_t* __restrict__ byte_off, int64_t n_seqs,
-                                                          int64_t base, uint32_t* __restrict__ words, int64_t cap,
-                                                          int64_t* __restrict__ word_off, int32_t* __restrict__ lens,
-                                                          unsigned long long* __restrict__ status) {
-    constexpr unsigned FULL = 0xffffffffu;
-    constexpr int B = 32 / BITS;  // bases per word
-    __shared__ uint8_t lut[256];
-    __shared__ int hist[8][33];
-    build_lut(lut, BITS);
-    __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t first = byte_off[0], total = byte_off[n_seqs];
-    if (total / B + n_seqs + base > cap) {  // capacity (closed-form layout): no writes at all
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(status, (unsigned long long)total);
-        return;
-    }
-    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x, nthr = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t sq = tid; sq < n_seqs; sq += nthr) {
-        const int64_t b0 = byte_off[sq];
-        word_off[sq] = b0 / B + sq + base;
-        if (lens) lens[sq] = int(byte_off[sq + 1] - b0);
-    }
-    if (tid == 0) word_off[n_seqs] = total / B + n_seqs + base;
-    if (total <= first) return;
-    // chunk j covers stream bytes [16 j - mis, 16 j - mis + 16): 16-byte aligned addresses
-    const int64_t mis = int64_t(reinterpret_cast<uintptr_t>(ascii) & 15u);
-    const int64_t j0 = (first + mis) >> 4, j1 = (total + mis + 15) >> 4;  // chunks [j0, j1)
-    const int64_t nwin = (j1 - j0 + 31) >> 5;
-    const int64_t warps = nthr >> 5, gw = tid >> 5;
-    const int64_t per = (nwin + warps - 1) / warps;
-    const int64_t win_lo = gw * per, win_hi = min(nwin, win_lo + per);
-    if (win_lo >= win_hi) return;
-    int64_t s0 = 0;  // sequence holding the current window's first byte (or the first sequence)
-    if (lane == 0) {
-        const int64_t w0 = 16 * (j0 + win_lo * 32) - mis, x = w0 > first ? w0 : first;
-        int64_t lo = 0, hi = n_seqs - 1;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) >> 1;
-            if (byte_off[mid] <= x) lo = mid;
-            else hi = mid - 1;
-        }
-        s0 = lo;
-    }
-    s0 = __shfl_sync(FULL, s0, 0);
-    for (int64_t win = win_lo; win < win_hi; ++win) {
-        const int64_t jw = j0 + win * 32;
-        const int64_t c0 = 16 * (jw + lane) - mis;  // my chunk's first stream byte
-        const int64_t w0 = 16 * jw - mis;           // the window's first stream byte
-        const int64_t bi = byte_off[min(s0 + 1 + lane, n_seqs)];  // end of sequence s0 + lane
-        uint32_t by[8];
-        auto load16 = [&](int64_t c, uint32_t* o) {
-            if (c >= first && c + 16 <= total) {
-                const uint4 v = __ldg(reinterpret_cast<const uint4*>(ascii + c));
-                o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
-            } else {  // batch edges: bytes outside [first, total) read as 'A'
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint32_t x = 0;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int64_t i = c + 4 * q + k;
-                        x |= uint32_t(i >= first && i < total ? ascii[i] : uint8_t('A')) << (8 * k);
-                    }
-                    o[q] = x;
-                }
-            }
-        };
-        load16(c0, by);
-        if (lane == 31) load16(c0 + 16, by + 4);
-        // codes: bit arithmetic per 8 ACGT bytes, the table otherwise
-        uint32_t code[4] = {0, 0, 0, 0};
-        uint32_t badmask = 0;
-        const int nhalf = lane == 31 ? 4 : 2;
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            if (h >= nhalf) break;
-            uint32_t nib = 0;
-            if (!fast_acgt8(make_uint2(by[2 * h], by[2 * h + 1]), nib)) {
-                uint32_t bad0 = 0, bad1 = 0;
-                const uint32_t inv = BITS == 4 ? 15u : 0u;
-                nib = lut_word(lut, by[2 * h], bad0, inv) | (lut_word(lut, by[2 * h + 1], bad1, inv) << 16);
-                if (h < 2) badmask |= (bad0 | (bad1 << 4)) << (8 * h);
-            }
-            if (BITS == 4) {
-                code[h] = nib;
-            } else {  // 8 nibbles (each <= 3) -> 8 two-bit fields
-                uint32_t t = nib;
-                t = (t | (t >> 2)) & 0x0F0F0F0Fu;
-                t = (t | (t >> 4)) & 0x00FF00FFu;
-                t = (t | (t >> 8)) & 0xFFFFu;
-                code[h >> 1] |= t << (16 * (h & 1));
-            }
-        }
-        if (badmask) {  // first invalid byte of my chunk inside the batch (PACK2: N included)
-            for (int k = 0; k < 16; ++k) {
-                const int64_t i = c0 + k;
-                if (((badmask >> k) & 1u) && i >= first && i < total) {
-                    atomicMin(status, (unsigned long long)i);
-                    break;
-                }
-            }
-        }
-        uint32_t nx0 = __shfl_down_sync(FULL, code[0], 1);  // the next chunk's first codes
-        if (lane == 31) nx0 = BITS == 4 ? code[2] : code[1];
-        // the sequence holding each lane's chunk start: boundaries at or before it, counted by lane
-        hist[wid][lane] = 0;
-        __syncwarp();
-        {
-            const int64_t k = (bi - w0 + 15) >> 4;  // first lane L with c0(L) >= bi
-            if (s0 + 1 + lane <= n_seqs && k <= 31) atomicAdd(&hist[wid][k < 0 ? 0 : int(k)], 1);
-        }
-        __syncwarp();
-        int cntL = hist[wid][lane];
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int v = __shfl_up_sync(FULL, cntL, off);
-            if (lane >= off) cntL += v;
-        }
-        const int64_t b31 = __shfl_sync(FULL, bi, 31);
-        int64_t s = s0 + cntL;
-        if (b31 <= c0 && s0 + 32 < n_seqs) {  // > 32 sequence ends before my chunk: search the rest
-            int64_t lo = s0 + 32, hi = n_seqs - 1;
-            while (lo < hi) {
-                const int64_t mid = (lo + hi + 1) >> 1;
-                if (byte_off[mid] <= c0) lo = mid;
-                else hi = mid - 1;
-            }
-            s = lo;
-        }
-        // the next window's first sequence: lane 31's, advanced past ends inside its chunk
-        int64_t sn = s;
-        // emit the words whose first byte is in my chunk [c0, c0 + 16)
-        for (; s < n_seqs; ++s) {
-            const int64_t st = byte_off[s], en = byte_off[s + 1];
-            if (st >= c0 + 16) break;
-            if (en <= c0 + 16) sn = s + 1;
-            if (en <= c0) continue;
-            int64_t w = st >= c0 ? 0 : (c0 - st + B - 1) / B;
-            const int64_t wbase = st / B + s + base;
-            for (int64_t b = st + B * w; b < en && b < c0 + 16; b += B, ++w) {
-                const int o = int(b - c0);  // 0..15
-                uint32_t val;
-                if (BITS == 4) {  // bits [4o, 4o + 32) of code[0] | code[1] << 32 | nx0 << 64
-                    const int k = 4 * o;
-                    val = k < 32 ? __funnelshift_r(code[0], code[1], k) : __funnelshift_r(code[1], nx0, k - 32);
-                    const int64_t nv = en - b;
-                    if (nv < 8) val |= 0xFFFFFFFFu << (4 * nv);
-                } else {
-                    val = __funnelshift_r(code[0], nx0, 2 * o);
-                    const int64_t nv = en - b;
-                    if (nv < 16) val &= (1u << (2 * nv)) - 1u;
-                }
-                words[wbase + w] = val;
-            }
-        }
-        s0 = __shfl_sync(FULL, sn < n_seqs ? sn : n_seqs - 1, 31);
-        __syncwarp();  // hist is rewritten by the next window
-    }
-}
-
 __global__ void status_init(unsigned long long* st) { *st = ~0ull >> 1; }
 __global__ void status_final(unsigned long long* st) {
     if (*st == (~0ull >> 1)) *st = (unsigned long long)(-1ll);
@@ -405,22 +222,12 @@ void launch_pack_range(const uint8_t* ascii, const int64_t* byte_off, int64_t n,
         const int64_t g8 = int64_t(sm_count_current()) * 8;
         const int64_t need = (n + 255) / 256;  // one warp per 32-sequence tile, 8 warps per block
         const int grid = int(need < g8 ? need : g8);
-#if SALOBA_PACK_TILE
         if (fmt == SALOBA_PACK4)
             pack_tile2_kernel<4><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, cap, word_off, lens,
                                                       (unsigned long long*)status);
         else
             pack_tile2_kernel<2><<<grid, 256, 0, s>>>(ascii, byte_off, n, base, words, cap, word_off, lens,
                                                       (unsigned long long*)status);
-#else
-        (void)grid;
-        if (fmt == SALOBA_PACK4)
-            pack_stream_kernel<4><<<int(g8), 256, 0, s>>>(ascii, byte_off, n, base, words, cap, word_off, lens,
-                                                          (unsigned long long*)status);
-        else
-            pack_stream_kernel<2><<<int(g8), 256, 0, s>>>(ascii, byte_off, n, base, words, cap, word_off, lens,
-                                                          (unsigned long long*)status);
-#endif
         count_launches(1);
     }
     launch_status_final(status, s);
