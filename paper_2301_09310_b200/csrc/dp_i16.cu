@@ -89,10 +89,10 @@ struct Stage {
 // of the block while this chunk runs.  `in` is the producer's progress word, `in_tag | blocks` once
 // `blocks` bottom-row blocks of the producing task are in global memory; `out` is this chunk's own.
 #ifndef COOP_PUB_CFG
-#define COOP_PUB_CFG 16
+#define COOP_PUB_CFG 8
 #endif
 #ifndef COOP_LAG_CFG
-#define COOP_LAG_CFG 48
+#define COOP_LAG_CFG 16
 #endif
 constexpr int COOP_PUB = COOP_PUB_CFG;  // bottom-row blocks per progress publication
 constexpr int COOP_LAG = COOP_LAG_CFG;  // extra blocks a chunk waits for before its first step
