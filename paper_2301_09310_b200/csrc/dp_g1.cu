@@ -250,12 +250,12 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
                 cp_async16s(s_ent + (slot * NS) * (G1_T * 16), g);
                 if (QN) cp_async16s(s_ent + (slot * NS + 1) * (G1_T * 16), g + G1_T);
             }
-            if (topA_mem && (!BAND || s2 <= bd.hiA)) {
+            if (topA_mem && (!BAND || (s2 <= bd.hiA && s2 >= bd.rbaseA))) {
                 const uint4* g = wide_at(g_topA, BAND ? s2 - bd.rbaseA : s2, str64);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) cp_async16s(s_ent + (T0 + slot * 4 + q) * (G1_T * 16), g + q);
             }
-            if (topB_mem && (!BAND || s2 <= bd.hiB)) {
+            if (topB_mem && (!BAND || (s2 <= bd.hiB && s2 >= bd.rbaseB))) {
                 const uint4* g = wide_at(g_topB, BAND ? s2 - bd.rbaseB : s2, str64);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) cp_async16s(s_ent + (T0 + (BOFF + slot) * 4 + q) * (G1_T * 16), g + q);
@@ -303,11 +303,14 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
             }
         }
         if (BAND) {  // top-row blocks the strip above never computed are out of band: H = F = 0
-            if (topA_mem && s2 > bd.hiA) {
+            // (and blocks before the first one it wrote: a split pass 2 starts at the union of both
+            // halves' ranges, which can precede one half's row; those are left of its band.  Read as
+            // garbage they reached the OTHER half through EXTEND's 32-bit lambda * hdiag IMAD carry.)
+            if (topA_mem && (s2 > bd.hiA || s2 < bd.rbaseA)) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) TOP(slot, q) = make_uint4(0, 0, 0, 0);
             }
-            if (PASS2 && split && topB_mem && s2 > bd.hiB) {
+            if (PASS2 && split && topB_mem && (s2 > bd.hiB || s2 < bd.rbaseB)) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) TOP(BOFF + slot, q) = make_uint4(0, 0, 0, 0);
             }
@@ -339,6 +342,13 @@ __device__ __forceinline__ uint32_t g1_strip(const AlignArgs& a, const int Q, co
             for (int r = 0; r < G1_R; ++r) {
                 Hl[r] = 0;
                 En[r] = nbeta;  // E(i, first band column) = max(0 - alpha, 0 - beta)
+            }
+            // the block is out of band for every row of the strip: its bottom row is H = F = 0
+            // (written, so every block of the row from its base on holds a value)
+            if (bot >= 0) {
+                uint4* g = wide_at(g_bot, s - bd.wbase, str64);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) st_global16(g + q, make_uint4(0u, 0u, 0u, 0u));
             }
             cur = (cur == DEPTH - 1) ? 0 : cur + 1;
             continue;

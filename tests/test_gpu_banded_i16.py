@@ -103,3 +103,22 @@ def test_small_batch_of_long_banded_reads_takes_int32(sb):
     got = gpu_banded(sb, b, w, sb.BWA_MEM, sb.LOCAL, sb.Options(bin_counts=bins))
     bc = bins.cpu().tolist()
     assert got[3] == -1 and bc[8] == 0 and sum(bc[0:8]) == b.n, bc
+
+
+def test_split_pass2_extend_halves_at_different_strips(sb):
+    """Regression (round-2 stress): a duo whose halves win in different strips (here strip 5 and
+    strip 0) runs pass 2 over the union of both band ranges, which starts before the first block the
+    strip above the later half ever wrote.  Those top-row blocks are left of its band and must read
+    as H = F = 0; read as stale memory they reached the other half through EXTEND's 32-bit
+    lambda * hdiag product (scheme 3/-2/7/3, w = 40, seeds as tools/repro_band.py found them)."""
+    import torch
+
+    full = synth.generate(2, 20000, seed=7, p_n=0.002)
+    full.h0[:] = np.random.default_rng(7).integers(1, 80, full.n).astype(np.int32)
+    b = full.subset([18510, 18511])
+    sc = sb.Scoring(3, -2, 7, 3)
+    w = np.full(b.n, 40, np.int32)
+    bins = torch.zeros(16, dtype=torch.int32, device="cuda")
+    got = gpu_banded(sb, b, w, sc, sb.EXTEND, sb.Options(force_path=2, keep_order=1, bin_counts=bins))
+    assert int(bins[8].item()) == 2
+    assert_same(got, oracle_banded(b, w, sc, oracle.EXTEND), b, w, "split pass 2")
